@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""Benchmark: SNN inference images/s on 1..8 B200 (+ NormAD training img/s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+Headline workload (BASELINE.json configs[2]): batched
+inference over the 10,000 synthetic MNIST-shaped images of
+synthetic_dataset(1000, seed=2000) (committed in data/workloads.npz, generated
+by the reference itself), weights W_fix, T=100 ms, dt=1 ms (100 steps),
+sharded contiguously over the ranks with one NCCL all-gather of the counts.
+One step = the whole 10,000-image set (strong scaling).  Rank 0 also times
+NormAD training (configs[1]: 1,000 images, one GPU) and, at N=1, the CPU
+reference (the oracle port, all host cores) on a bounded sample.
+
+--impl reference times the reference's CPU algorithm (oracle/snn_oracle.py,
+a bit-exact numpy restatement of spikedigits) on the host cores instead.
+"""
+from __future__ import annotations
+
+import os
+
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import argparse
+import ctypes
+import json
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SNN inference images/sec @1/2/4/8 B200 + NormAD train img/s, % roofline vs CPU ref"
+N_IMAGES = 10_000
+F_INF_PER_STEP = 389_516          # dense algorithmic flop per image-step
+F_TRAIN_PER_STEP = 592_316
+F_TRAIN_PER_IMAGE = 162_240
+# executed float64 flop per ACTIVE window position and step in k_hidden:
+# 12 features x (1 mul + 8 FMA = 17 flop stencil + 5 flop LIF update)
+FLOP_PER_ACTIVE_POS_STEP = 12 * (17 + 5)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measure_peaks():
+    """FP64 DFMA / FP32 FFMA peaks of this GPU (libsnn_peaks.so microbenchmark)."""
+    from paper_1711_03637_b200.build import PEAKS_OUT
+    lib = ctypes.CDLL(PEAKS_OUT)
+    f64, f32 = ctypes.c_double(), ctypes.c_double()
+    best64 = best32 = 0.0
+    for _ in range(3):
+        lib.snn_measure_fma_peaks(ctypes.byref(f64), ctypes.byref(f32))
+        best64, best32 = max(best64, f64.value), max(best32, f32.value)
+    return best64, best32
+
+
+def active_positions(images: np.ndarray) -> np.ndarray:
+    """Windows with any non-zero pixel, per image (the ones k_hidden simulates)."""
+    nz = images.reshape(-1, 28, 28) != 0
+    win = np.zeros((len(images), 26, 26), dtype=bool)
+    for a in range(3):
+        for b in range(3):
+            win |= nz[:, a:a + 26, b:b + 26]
+    return win.reshape(len(images), -1).sum(axis=1)
+
+
+def load_workload():
+    d = np.load(os.path.join(ROOT, "data", "workloads.npz"))
+    w = np.load(os.path.join(ROOT, "data", "w_fix.npz"))["w_fix"]
+    return d, w
+
+
+# ============================================================== reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import snn_oracle as orc
+    d, w = load_workload()
+    imgs = d["c3_images"]
+    cores = host_cores()
+    p = orc.Params()
+    sample = int(min(len(imgs), max(2 * cores, cores * 8)))
+    log(f"[reference] oracle port on {cores} cores, {sample} images per step")
+    for _ in range(args.warmup):
+        orc.batch_counts(imgs[:sample], w, p, workers=cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        orc.batch_counts(imgs[:sample], w, p, workers=cores)
+        times.append(time.perf_counter() - t0)
+    value = sample * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference strokes generator)",
+        "config": {"workload": "c3 batched inference (reference CPU algorithm), bounded sample",
+                   "n_images_per_step": sample, "t_ms": 100.0, "dt_ms": 1.0, "n_steps": 100,
+                   "parallelism": f"{cores} host processes"},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
+                         "sample": f"first {sample} of the 10,000 c3 images per step, "
+                                   f"oracle.batch_counts(workers={cores}), {cpu_model()}"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ============================================================== our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1711_03637_b200 as sd
+    from paper_1711_03637_b200 import distributed as sdist
+    from paper_1711_03637_b200.engine import get_engine, make_consts
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    d, w_fix = load_workload()
+    imgs_all = d["c3_images"]
+    cfg, bank = sd.NetworkConfig(), sd.default_filter_bank()
+    c = make_consts(cfg, bank)
+    eng = get_engine()
+    a, b = sdist.shard_bounds(N_IMAGES, world)[rank]
+    shard = imgs_all[a:b].reshape(b - a, -1)
+    with torch.cuda.stream(eng.stream):
+        d_img = torch.from_numpy(shard.copy()).to(eng.device)
+        d_w = torch.from_numpy(w_fix.copy()).to(eng.device)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=eng.device)
+    eng.stream.synchronize()
+    per_img_ws = eng.lib.snn_infer_workspace(ctypes.byref(c), 1)
+    chunk = max(1, min(b - a, (1 << 30) // per_img_ws))
+    launches_per_step = -(-(b - a) // chunk)
+
+    def step():
+        out = eng.infer(c, d_img, d_w)["counts"]
+        with torch.cuda.stream(eng.stream):
+            return sdist.gather_counts(out, N_IMAGES) if world > 1 else out
+
+    for _ in range(args.warmup):
+        step()
+    eng.stream.synchronize()
+    barrier()
+
+    step_ms, kern_ms = [], []
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        for _ in range(args.steps):
+            with torch.cuda.stream(eng.stream):
+                flush.zero_()               # evict the 7.8 MB input set from the 126 MB L2
+            e0, k1, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(eng.stream)
+            out = eng.infer(c, d_img, d_w)["counts"]
+            k1.record(eng.stream)
+            if world > 1:
+                with torch.cuda.stream(eng.stream):
+                    out = sdist.gather_counts(out, N_IMAGES)
+            e1.record(eng.stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            kern_ms.append(e0.elapsed_time(k1))
+        torch.cuda.synchronize()
+        barrier()
+    clocks = clk.summary()
+    tot_ms, ker_ms = max_over_ranks([sum(step_ms), sum(kern_ms)])
+    value = N_IMAGES * args.steps / (tot_ms / 1e3)
+    counts_dev = out
+    ref_prefix = None
+    if rank == 0:
+        gold = np.load(os.path.join(ROOT, "tests", "golden", "reference_golden.npz"))["c3_counts_200"]
+        ref_prefix = bool(np.array_equal(counts_dev[:200].cpu().numpy(), gold)) if counts_dev.shape[0] >= 200 else None
+
+    # ---- e2e: public API with host buffers (H2D images + weights, D2H counts)
+    e2e_times = []
+    for i in range(args.warmup + args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        res = sdist.sharded_batch_counts(imgs_all, w_fix, bank, cfg)
+        dt_s = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_times.append(dt_s)
+    (e2e_s,) = max_over_ranks([sum(e2e_times)])
+    e2e_value = N_IMAGES * args.steps / e2e_s
+    h2d = (b - a) * 784 + w_fix.nbytes
+    d2h = N_IMAGES * 10 * 4
+
+    line = None
+    if rank == 0:
+        f64, f32 = measure_peaks()
+        act = active_positions(shard.reshape(-1, 28, 28))
+        n_steps = c.n_steps
+        launch_ms = ker_ms / (args.steps * launches_per_step)
+        exec_flop_launch = float(act.sum()) * n_steps * FLOP_PER_ACTIVE_POS_STEP / launches_per_step
+        achieved = exec_flop_launch / (launch_ms * 1e-3) / 1e12
+        dense_tflops = (b - a) * F_INF_PER_STEP * n_steps / (ker_ms / args.steps * 1e-3) / 1e12
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: reference stroke generator images (data/workloads.npz), reference-trained W_fix",
+            "config": {"workload": "c3: batched inference, 10,000 synthetic MNIST-shaped 28x28 images, "
+                                   "12x3x3 feature maps (8112 LIF) -> 10 LIF, T=100 ms, dt=1 ms",
+                       "n_images": N_IMAGES, "t_ms": 100.0, "dt_ms": 1.0, "n_steps": n_steps,
+                       "parallelism": f"dp{world}", "collective": "one NCCL all_gather of int32 counts"
+                       if world > 1 else "none", "l2": "flushed between timed steps (256 MiB write)"},
+            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "api": "distributed.sharded_batch_counts (host numpy in/out)"},
+            "gpu_launches": int(args.steps * launches_per_step),
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": f64, "unit": "TFLOP/s",
+                         "frac": achieved / f64, "traffic": None,
+                         "kernel": "k_hidden<GSUM> (stencil + hidden LIF + event-driven contraction + output layer)",
+                         "achieved_basis": f"executed fp64 flop: active windows x N x {FLOP_PER_ACTIVE_POS_STEP}",
+                         "peak_source": "measured in this run: FP64 DFMA microbenchmark (libsnn_peaks.so); "
+                                        "MEASURED_PEAKS.json has no FP64 figure",
+                         "launch_ms": launch_ms, "dense_equiv_tflops": dense_tflops,
+                         "dense_equiv_basis": "SURVEY 8(d) F_inf = 389,516 flop per image-step",
+                         "fp32_peak_tflops": f32, "active_windows_per_image": float(act.mean())},
+            "clocks": clocks,
+            "parity": {"c3_first200_counts_equal_reference": ref_prefix},
+        }
+    # ---- NormAD training (single GPU, rank 0)
+    if rank == 0 and not args.skip_train:
+        line["train"] = bench_train(args, sd, eng, d, cfg, bank)
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        line["cpu_baseline"] = cpu_baseline(d, w_fix)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    barrier()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bench_train(args, sd, eng, d, cfg, bank):
+    import torch
+    from paper_1711_03637_b200.engine import make_consts
+    learn = sd.LearnConfig()
+    order = d["c2_order"]
+    imgs = d["c2_images"][order].reshape(len(order), -1)
+    labs = d["c2_labels"][order].astype(np.uint8)
+    c = make_consts(cfg, bank, learn)
+    with torch.cuda.stream(eng.stream):
+        d_img = torch.from_numpy(imgs.copy()).to(eng.device)
+        d_lab = torch.from_numpy(labs.copy()).to(eng.device)
+        d_w = torch.zeros((8112, 10), dtype=torch.float64, device=eng.device)
+    eng.train(c, d_img, d_lab, d_w)
+    times = []
+    for _ in range(max(2, min(args.steps, 3))):
+        d_w.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(eng.stream)
+        _, status = eng.train(c, d_img, d_lab, d_w)
+        e1.record(eng.stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    n = len(order)
+    value = n / (statistics.median(times) / 1e3)
+    wf = np.load(os.path.join(ROOT, "data", "w_fix.npz"))["w_fix"]
+    rel = float(np.abs(d_w.cpu().numpy() - wf).max() / np.abs(wf).max())
+    # e2e: train_epoch API from host arrays (weights H2D + D2H included)
+    t0 = time.perf_counter()
+    w_api, stats = sd.train_epoch(d["c2_images"][order], d["c2_labels"][order], sd.zero_weights(), bank, cfg, learn)
+    e2e = n / (time.perf_counter() - t0)
+    # CPU reference: the oracle port's train_epoch (one core, as the reference trains) on 30 images
+    from oracle import snn_oracle as orc
+    k = 30
+    t0 = time.perf_counter()
+    orc.train_epoch(d["c2_images"][order][:k], d["c2_labels"][order][:k], np.zeros((8112, 10)), orc.Params())
+    cpu = k / (time.perf_counter() - t0)
+    return {"metric": "NormAD online training images/s (1 GPU, sequential)", "value": value, "unit": "images/s",
+            "workload": "c2: 1,000 synthetic images in epoch_permutation(0,0,1000) order from zero weights, "
+                        "T=100 ms, dt=1 ms, lr=2e-7", "ms_per_epoch": statistics.median(times),
+            "e2e": {"value": e2e, "unit": "images/s", "api": "train_epoch (host numpy in/out)"},
+            "w_rel_err_vs_reference_epoch": rel, "train_errors": stats.n_errors,
+            "dense_equiv_tflops": value * (F_TRAIN_PER_STEP * 100 + F_TRAIN_PER_IMAGE) / 1e12,
+            "gpu_launches_per_epoch": 3 * 1,
+            "cpu_baseline": {"value": cpu, "unit": "images/s", "cores": 1, "kind": "port",
+                             "sample": f"oracle.train_epoch on the first {k} images (1 core, as the reference)"}}
+
+
+def cpu_baseline(d, w):
+    from oracle import snn_oracle as orc
+    cores = host_cores()
+    imgs = d["c3_images"]
+    sample = int(min(len(imgs), max(2 * cores, cores * 16)))
+    p = orc.Params()
+    orc.batch_counts(imgs[: 2 * cores], w, p, workers=cores)  # fork + table warm-up
+    t0 = time.perf_counter()
+    orc.batch_counts(imgs[:sample], w, p, workers=cores)
+    v = sample / (time.perf_counter() - t0)
+    return {"value": v, "unit": "images/s", "cores": cores, "kind": "port",
+            "sample": f"first {sample} of the 10,000 c3 images, oracle.batch_counts(workers={cores}), {cpu_model()}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--skip-train", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

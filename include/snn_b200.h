@@ -1,0 +1,124 @@
+/*
+ * snn_b200.h -- C ABI of the B200-native spiking-digit hot path.
+ *
+ * Drop-in boundary for the reference package `spikedigits`
+ * (/root/reference/pkg/src/spikedigits).  The reference has no FFI: its hot
+ * path sits behind Python functions, and each entry point below is what the
+ * Python API mirror (paper_1711_03637_b200/) binds through ctypes to replace
+ * one of them (see INTEGRATION.md for the bindings):
+ *
+ *   snn_input_table  <- network._input_tables           (network.py:224-245)
+ *   snn_infer        <- network.run_presentation         (network.py:267-326)
+ *                       network.forward_pass             (network.py:329-346)
+ *                       evaluate.batch_counts            (evaluate.py:27-40)
+ *   snn_train        <- normad.train_presentation        (normad.py:141-162)
+ *                       normad.train_epoch               (normad.py:179-207)
+ *
+ * Conventions: all array pointers are DEVICE pointers owned by the caller;
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ * asynchronous on `stream` except where noted.  Arithmetic is IEEE float64
+ * in the reference's SI units and operation order.  No torch types cross
+ * this boundary.
+ */
+#ifndef SNN_B200_H
+#define SNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SNN_ABI_VERSION 1
+
+#define SNN_IMAGE_SIDE 28
+#define SNN_N_PIXELS 784
+#define SNN_N_FILTERS 12
+#define SNN_N_POSITIONS 676 /* 26 x 26 valid windows */
+#define SNN_N_HIDDEN 8112   /* (row*26+col)*12 + filter, network.py:158 */
+#define SNN_N_OUTPUTS 10
+#define SNN_TILE 32          /* window positions per warp tile */
+#define SNN_MAX_TILES 22     /* ceil(676 / 32) */
+
+/* status codes (int return values and d_status[0]) */
+#define SNN_OK 0
+#define SNN_ENOMEM 12
+#define SNN_EINVAL 22
+#define SNN_ENONFINITE 1001 /* weight update produced non-finite values (normad.py:122-124) */
+#define SNN_ECUDA 1002
+
+/* One LIF population, derived on the host exactly as neurons.lif_step does
+ * (neurons.py:109-118): beta = dt*(2 - g*dt/C)/(2*C), refr = t_ref/dt. */
+typedef struct snn_lif {
+    double g;    /* leak conductance, S */
+    double el;   /* rest / reset potential, V */
+    double vt;   /* threshold, V */
+    double beta; /* RK2 collapsed step factor */
+    double refr; /* refractory / dt (float64, compared as step > last + refr) */
+} snn_lif_t;
+
+/* Everything the hot path reads from NetworkConfig / FilterBank / LearnConfig.
+ * Decay factors are host libm exp() values (neurons.py:148-150, normad.py:82). */
+typedef struct snn_consts {
+    int32_t n_steps;        /* round(T/dt), network.py:148-150 */
+    int32_t desired_period; /* steps between target spikes; 0 = no target (network.py:171-193) */
+    double dt;
+    double i0, ip;          /* pixel encoding i = i0 + k*ip (network.py:72-77) */
+    snn_lif_t lif_in, lif_hid, lif_out;
+    double decay_slow;      /* exp(-dt/5 ms)  */
+    double decay_fast;      /* exp(-dt/1.25 ms) */
+    double decay_learn;     /* exp(-dt/1 ms), normad.py:82 */
+    double dhat_scale;      /* dt / C_out, normad.py:83 */
+    double inhibition;      /* NetworkConfig.inhibition_weight (A per unit trace) */
+    double learning_rate;   /* LearnConfig.learning_rate */
+    double norm_eps;        /* LearnConfig.norm_epsilon */
+    double taps[12][9];     /* FilterBank.weighted[f].ravel() (filters.py:57-60) */
+} snn_consts_t;
+
+/* Optional outputs of snn_infer; every pointer may be NULL except counts. */
+typedef struct snn_infer_out {
+    int32_t *counts;     /* [n][10] output spike counts */
+    uint16_t *raster;    /* [n][22][N][32] per-lane 12-bit hidden spike masks */
+    uint16_t *tile_pos;  /* [n][22][32] window position of each lane (0xFFFF = none) */
+    int32_t *n_tiles;    /* [n] live tiles per image */
+    uint16_t *out_raster;/* [n][N] 10-bit output spike masks */
+    double *ff;          /* [n][N][10] feed-forward current c_hidden @ W */
+    double *v_out;       /* [n][N][10] output membrane after each step */
+    double *v_hid;       /* [n][N][8112] hidden membrane after each step (only
+                            neurons of live windows are written) */
+} snn_infer_out_t;
+
+int snn_abi_version(void);
+const char *snn_last_error(void);
+
+/* Input-layer response table for the 256 pixel levels (replaces the
+ * lru-cached network._input_tables).  d_ctab: [N][256] float64 kernel traces;
+ * d_spk: [N][256] uint8 spike flags (may be NULL). */
+int snn_input_table(const snn_consts_t *c, double *d_ctab, uint8_t *d_spk, void *stream);
+
+/* Bytes of device workspace snn_infer needs for n images. */
+size_t snn_infer_workspace(const snn_consts_t *c, int64_t n_images);
+
+/* Batched inference: n independent presentations (uint8 [n][784] images,
+ * float64 [8112][10] row-major weights, table from snn_input_table). */
+int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t n_images,
+              const double *d_weights, const double *d_ctab, const snn_infer_out_t *out,
+              void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* Bytes of device workspace snn_train needs for n images. */
+size_t snn_train_workspace(const snn_consts_t *c, int64_t n_images);
+
+/* Sequential online NormAD over n images in the given order, updating
+ * d_weights in place (float64 [8112][10]).  d_counts: [n][10] pre-update
+ * output counts.  d_status (int32[4], device): [0] status code, [1] index of
+ * the failing image, [2] images completed.  On SNN_ENONFINITE the weights hold
+ * the state before the failing image (the reference raises and discards it). */
+int snn_train(const snn_consts_t *c, const uint8_t *d_images, const uint8_t *d_labels,
+              int64_t n_images, double *d_weights, const double *d_ctab, int32_t *d_counts,
+              int32_t *d_status, void *d_workspace, size_t workspace_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNN_B200_H */

@@ -1,0 +1,331 @@
+// NormAD online training (normad.py:141-207) on sm_100a.
+//
+// The reference runs, per image, the whole network step by step and calls a
+// hook that filters the hidden kernel traces into d_hat, compares output and
+// target spikes and accumulates the normalised update (normad.py:156-159).
+// Only the 10-neuron output layer couples to the weights, so the trial splits
+// into a weight-independent part that runs ahead for a whole chunk of images
+// in parallel, and a short weight-dependent part that must run image after
+// image (W_{i+1} = W_i + r * dW_i):
+//
+//   K1 k_hidden<RASTER>   (parallel)  hidden spike raster per image
+//   K2 k_compact          (parallel)  active-neuron list, per-neuron spike
+//                                     lists, per-step spike lists (CSR), and
+//                                     the d_hat norm of every step
+//   K3 k_normad           (sequential, one CTA, loops over the images)
+//        G(s,l)  = sum of W rows of hidden neurons spiking at s
+//        scan    = output layer + error signal + gate; sigma(s,l) = e*dt/|d_hat|
+//        R(u,l)  = sum_{s>=u} sigma(s,l) H(s-u), H = d_hat response of one spike
+//        dW[k,l] = sum over spikes u of neuron k of R(u,l);  W += r*dW
+//
+// d_hat_k(s) = sum_{u<=s} H(s-u) over k's spikes (both trace recursions are
+// linear), hence dW[k,l] = sum_s d_hat_k(s) sigma(s,l) = sum_u R(u,l): the
+// event-driven form touches only the ~7k spikes of an image instead of the
+// dense 8112 x N trace.  All sums run in a fixed order (deterministic).
+#pragma once
+#include "hidden.cuh"
+
+namespace snn {
+
+constexpr int kCThreads = kMaxTiles * 32;  // 704: one thread per (tile, lane) slot
+constexpr int kTThreads = 1024;            // sequential NormAD CTA
+
+struct TrainWS {
+    uint16_t *raster;   // [n][22][N][32]
+    uint16_t *tile_pos; // [n][22][32]
+    int32_t *n_tiles;   // [n]
+    int32_t *n_act;     // [n]
+    uint16_t *act_k;    // [n][8112]  active neuron ids, ascending
+    int32_t *act_off;   // [n][8113]  per active neuron: start in nsp
+    uint16_t *nsp;      // [n][evcap] spike steps per active neuron
+    int32_t *step_off;  // [n][N+1]   per step: start in step_k
+    uint16_t *step_k;   // [n][evcap] spiking neuron ids per step, ascending
+    double *norm;       // [n][N]     |d_hat(s)|
+    double *wp;         // [n][22][N] per-warp partial sums of d_hat^2
+    int64_t evcap;
+};
+
+struct TrainArgs {
+    snn_consts_t c;
+    TrainWS ws;
+    const uint8_t *labels;  // chunk-relative
+    double *w;
+    int32_t *counts;        // chunk-relative [n][10]
+    int32_t *status;        // [4]
+    int64_t n;              // images in this chunk
+    int64_t first;          // absolute index of the chunk's first image
+};
+
+__device__ __forceinline__ uint64_t warp_incl_scan(uint64_t x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+// Exclusive block scan of uint64 (callers alternate two 32-entry buffers).
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t x, uint64_t *buf, uint64_t *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint64_t inc = warp_incl_scan(x);
+    if (lane == 31) buf[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t t = lane < nw ? buf[lane] : 0;
+        t = warp_incl_scan(t);
+        if (lane < nw) buf[lane] = t;
+    }
+    __syncthreads();
+    *total = buf[nw - 1];
+    return (warp ? buf[warp - 1] : 0) + inc - x;
+}
+
+__device__ __forceinline__ double warp_sum_fixed(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_xor_sync(kFull, x, o));
+    return x;
+}
+
+// ---------------------------------------------------------------------------
+// K2: per image, lists + d_hat norms.  grid = n, block = 704.
+__global__ void __launch_bounds__(kCThreads) k_compact(const TrainArgs T) {
+    __shared__ uint64_t s_buf[2][32];
+    const int tid = threadIdx.x, lane = tid & 31, tile = tid >> 5;
+    const int64_t img = blockIdx.x;
+    const int N = T.c.n_steps;
+    const TrainWS &W = T.ws;
+    const int ntiles = W.n_tiles[img];
+    int pos = 0xFFFF;
+    if (tile < ntiles) pos = W.tile_pos[((size_t)img * kMaxTiles + tile) * kTile + lane];
+    const bool valid = pos != 0xFFFF;
+    const uint16_t *R = W.raster + ((size_t)img * kMaxTiles + tile) * N * kTile + lane;
+
+    // pass 1: which of my 12 neurons ever fire, and how often
+    unsigned ever = 0;
+    int cnt[kNF];
+#pragma unroll
+    for (int f = 0; f < kNF; ++f) cnt[f] = 0;
+    if (valid)
+        for (int s = 0; s < N; ++s) {
+            const unsigned m = R[(size_t)s * kTile];
+            ever |= m;
+#pragma unroll
+            for (int f = 0; f < kNF; ++f) cnt[f] += (m >> f) & 1u;
+        }
+    int ev = 0;
+#pragma unroll
+    for (int f = 0; f < kNF; ++f) ev += cnt[f];
+    constexpr uint64_t kLow = (1ull << 40) - 1;
+    uint64_t tot;
+    const uint64_t ex = block_excl_scan(((uint64_t)__popc(ever) << 40) | (uint64_t)ev, s_buf[0], &tot);
+    const int n_act = (int)(tot >> 40);
+    const int64_t n_ev = (int64_t)(tot & kLow);
+    uint16_t *act_k = W.act_k + (size_t)img * kNH;
+    int32_t *act_off = W.act_off + (size_t)img * (kNH + 1);
+    uint16_t *nsp = W.nsp + (size_t)img * W.evcap;
+    uint16_t *step_k = W.step_k + (size_t)img * W.evcap;
+    int32_t *step_off = W.step_off + (size_t)img * (N + 1);
+    if (n_ev > W.evcap) {  // cannot happen with the worst-case capacity; fail loudly
+        if (tid == 0) atomicCAS(T.status, 0, SNN_ENOMEM);
+        return;
+    }
+    if (tid == 0) {
+        W.n_act[img] = n_act;
+        act_off[n_act] = (int32_t)n_ev;
+    }
+    int cursor[kNF];
+    {
+        int r = (int)(ex >> 40), e = (int)(ex & kLow);
+#pragma unroll
+        for (int f = 0; f < kNF; ++f) {
+            cursor[f] = e;
+            if ((ever >> f) & 1u) {
+                act_k[r] = (uint16_t)(pos * kNF + f);
+                act_off[r] = e;
+                ++r;
+                e += cnt[f];
+            }
+        }
+    }
+
+    // pass 2: per-step CSR (4 steps per packed scan) and per-neuron spike steps
+    int step_base = 0, parity = 1;
+    for (int s0 = 0; s0 < N; s0 += 4) {
+        unsigned ms[4];
+        uint64_t pk = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int s = s0 + q;
+            ms[q] = (valid && s < N) ? (unsigned)R[(size_t)s * kTile] : 0u;
+            pk |= (uint64_t)__popc(ms[q]) << (16 * q);
+        }
+        uint64_t t4;
+        const uint64_t ex4 = block_excl_scan(pk, s_buf[parity], &t4);
+        parity ^= 1;
+        int before = step_base;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int s = s0 + q;
+            if (s < N) {
+                if (tid == 0) step_off[s] = before;
+                int o = before + (int)((ex4 >> (16 * q)) & 0xFFFF);
+                const unsigned m = ms[q];
+#pragma unroll
+                for (int f = 0; f < kNF; ++f)
+                    if ((m >> f) & 1u) {
+                        step_k[o++] = (uint16_t)(pos * kNF + f);
+                        nsp[cursor[f]++] = (uint16_t)s;
+                    }
+            }
+            before += (int)((t4 >> (16 * q)) & 0xFFFF);
+        }
+        step_base = before;
+    }
+    if (tid == 0) step_off[N] = step_base;
+    __syncthreads();
+
+    // pass 3: |d_hat(s)|^2 = sum_k d_hat_k(s)^2 over the active neurons, replaying
+    // each neuron's kernel and d_hat recursions exactly as normad.py:82-83 /
+    // neurons.py:169-171 do.  Fixed reduction order: per-warp butterfly, then
+    // warps in index order.
+    double *wp = W.wp + (size_t)img * kMaxTiles * N;
+    const double lam1 = T.c.decay_slow, lam2 = T.c.decay_fast, lamL = T.c.decay_learn, kap = T.c.dhat_scale;
+    for (int base = 0; base < n_act || base == 0; base += kCThreads) {
+        const int j = base + tid;
+        const bool ok = j < n_act;
+        int e0 = ok ? act_off[j] : 0;
+        const int e1 = ok ? act_off[j + 1] : 0;
+        int nxt = e0 < e1 ? (int)nsp[e0] : 0x7fffffff;
+        double a = 0.0, b = 0.0, d = 0.0;
+        for (int s = 0; s < N; ++s) {
+            const bool sp = s == nxt;
+            if (sp) {
+                ++e0;
+                nxt = e0 < e1 ? (int)nsp[e0] : 0x7fffffff;
+            }
+            const double bump = sp ? 1.0 : 0.0;
+            a = __dadd_rn(__dmul_rn(a, lam1), bump);
+            b = __dadd_rn(__dmul_rn(b, lam2), bump);
+            const double c = __dsub_rn(a, b);
+            d = __dadd_rn(__dmul_rn(d, lamL), __dmul_rn(c, kap));
+            const double x = warp_sum_fixed(ok ? __dmul_rn(d, d) : 0.0);
+            if (lane == 0) wp[(size_t)tile * N + s] = base == 0 ? x : __dadd_rn(wp[(size_t)tile * N + s], x);
+        }
+        if (base + kCThreads >= n_act) break;
+    }
+    __syncthreads();
+    double *nrm = W.norm + (size_t)img * N;
+    for (int s = tid; s < N; s += kCThreads) {
+        double q = 0.0;
+        for (int w = 0; w < kMaxTiles; ++w) q = __dadd_rn(q, wp[(size_t)w * N + s]);
+        nrm[s] = __dsqrt_rn(q);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: the sequential part, one CTA walking the chunk's images in order.
+// dynamic smem: GR[N*10] (G, then R) | SIG[N*10] | H[N] | flags
+__global__ void __launch_bounds__(kTThreads) k_normad(const TrainArgs T) {
+    extern __shared__ __align__(16) double smem[];
+    const int N = T.c.n_steps;
+    double *GR = smem;
+    double *SIG = GR + (size_t)N * kNO;
+    double *H = SIG + (size_t)N * kNO;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const snn_consts_t &c = T.c;
+    const TrainWS &W = T.ws;
+
+    if (T.status[0] != 0) return;  // an earlier chunk failed
+    if (tid == 0) {
+        // d_hat response to one hidden spike at lag m (kernel then d_hat filter)
+        double a = 0.0, b = 0.0, d = 0.0;
+        for (int m = 0; m < N; ++m) {
+            const double bump = m == 0 ? 1.0 : 0.0;
+            a = __dadd_rn(__dmul_rn(a, c.decay_slow), bump);
+            b = __dadd_rn(__dmul_rn(b, c.decay_fast), bump);
+            d = __dadd_rn(__dmul_rn(d, c.decay_learn), __dmul_rn(__dsub_rn(a, b), c.dhat_scale));
+            H[m] = d;
+        }
+    }
+    __syncthreads();
+
+    for (int64_t i = 0; i < T.n; ++i) {
+        const int32_t *soff = W.step_off + (size_t)i * (N + 1);
+        const uint16_t *sk = W.step_k + (size_t)i * W.evcap;
+        // (1) G(s,l): sum of W rows over the step's spiking neurons, ascending id
+        for (int t = tid; t < N * kNO; t += kTThreads) {
+            const int s = t / kNO, l = t - s * kNO;
+            double g = 0.0;
+            const int e1 = soff[s + 1];
+            for (int e = soff[s]; e < e1; ++e) g = __dadd_rn(g, __ldcg(T.w + (size_t)sk[e] * kNO + l));
+            GR[t] = g;
+        }
+        __syncthreads();
+        // (2) output layer + error signal + NormAD gate (normad.py:156-159, :104-113)
+        if (warp == 0) {
+            const int l = lane < kNO ? lane : kNO - 1;
+            const int label = T.labels[i];
+            const int per = c.desired_period;
+            const double *nrm = W.norm + (size_t)i * N;
+            OutState st;
+            out_init(st, c);
+            for (int s = 0; s < N; ++s) {
+                double ff;
+                const bool fired = out_step(st, c, GR[s * kNO + l], s, &ff);
+                const bool want = per > 0 && l == label && s >= per - 1 && (s - (per - 1)) % per == 0;
+                const int e = (int)want - (int)fired;
+                const bool any = (__ballot_sync(kFull, lane < kNO && e != 0) != 0);
+                const double nv = nrm[s];
+                double sg = 0.0;
+                if (any && nv > c.norm_eps && e != 0) sg = __ddiv_rn(__dmul_rn((double)e, c.dt), nv);
+                if (lane < kNO) SIG[s * kNO + lane] = sg;
+            }
+            if (lane < kNO) T.counts[(size_t)i * kNO + lane] = st.cnt;
+        }
+        __syncthreads();
+        // (3) R(u,l) = sum_{s>=u} sigma(s,l) H(s-u)
+        for (int t = tid; t < N * kNO; t += kTThreads) {
+            const int u = t / kNO, l = t - u * kNO;
+            double r = 0.0;
+            for (int s = u; s < N; ++s) {
+                const double sg = SIG[s * kNO + l];
+                if (sg != 0.0) r = __dadd_rn(r, __dmul_rn(sg, H[s - u]));
+            }
+            GR[t] = r;
+        }
+        __syncthreads();
+        // (4) dW and the update W + r*dW (normad.py:117-127), all-or-nothing
+        const int n_act = W.n_act[i];
+        const uint16_t *act_k = W.act_k + (size_t)i * kNH;
+        const int32_t *act_off = W.act_off + (size_t)i * (kNH + 1);
+        const uint16_t *nsp = W.nsp + (size_t)i * W.evcap;
+        for (int pass = 0; pass < 2; ++pass) {
+            bool bad = false;
+            for (int t = tid; t < n_act * kNO; t += kTThreads) {
+                const int j = t / kNO, l = t - j * kNO;
+                double acc = 0.0;
+                const int e1 = act_off[j + 1];
+                for (int e = act_off[j]; e < e1; ++e) acc = __dadd_rn(acc, GR[(int)nsp[e] * kNO + l]);
+                double *wp = T.w + (size_t)act_k[j] * kNO + l;
+                const double wn = __dadd_rn(__ldcg(wp), __dmul_rn(c.learning_rate, acc));
+                if (pass == 0) bad |= !isfinite(wn);
+                else *wp = wn;
+            }
+            if (pass == 0) {
+                if (__syncthreads_or(bad)) {
+                    if (tid == 0) {
+                        T.status[0] = SNN_ENONFINITE;
+                        T.status[1] = (int32_t)(T.first + i);
+                    }
+                    return;
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) T.status[2] = (int32_t)(T.first + i + 1);
+    }
+}
+
+}  // namespace snn

@@ -1,0 +1,52 @@
+// Pipe-peak microbenchmarks for the roofline denominators (not product code).
+// MEASURED_PEAKS.json carries HBM and bf16 tensor peaks only; the SNN kernels
+// are bound by the FP64 (and integer/ALU) pipes, so bench.py measures the
+// FP64 DFMA and FP32 FFMA peaks on the box in the same run.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+template <typename T, int CH>
+__global__ void __launch_bounds__(256) k_fma_peak(T *out, int iters, T a, T b) {
+    T x[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = (T)(threadIdx.x + c);
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int c = 0; c < CH; ++c) x[c] = x[c] * a + b;
+    T s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s += x[c];
+    if (s == (T)-1.2345) out[0] = s;  // keep the chains alive
+}
+
+template <typename T>
+static double run(int iters) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    T *out;
+    cudaMalloc(&out, sizeof(T));
+    const int blocks = sms * 8, threads = 256;
+    constexpr int CH = 8;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_fma_peak<T, CH><<<blocks, threads>>>(out, iters / 4, (T)0.999, (T)1e-3);  // warm-up
+    cudaEventRecord(e0);
+    k_fma_peak<T, CH><<<blocks, threads>>>(out, iters, (T)0.999, (T)1e-3);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaFree(out);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 2.0 * CH * (double)iters * blocks * threads;
+    return flops / (ms * 1e-3) / 1e12;
+}
+
+extern "C" int snn_measure_fma_peaks(double *tflops_fp64, double *tflops_fp32) {
+    *tflops_fp64 = run<double>(1 << 14);
+    *tflops_fp32 = run<float>(1 << 15);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1002;
+}

@@ -1,0 +1,201 @@
+// C ABI of the spiking-digit hot path (include/snn_b200.h).  One translation
+// unit: the kernels live in hidden.cuh (inference) and normad.cuh (training).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "normad.cuh"
+
+using namespace snn;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int set_error(int code, const char *msg) {
+    snprintf(g_err, sizeof(g_err), "%s", msg);
+    return code;
+}
+
+int cuda_check(const char *where) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        char buf[512];
+        snprintf(buf, sizeof(buf), "%s: %s", where, cudaGetErrorString(e));
+        return set_error(SNN_ECUDA, buf);
+    }
+    return SNN_OK;
+}
+
+int validate(const snn_consts_t *c) {
+    if (!c) return set_error(SNN_EINVAL, "consts is NULL");
+    if (c->n_steps <= 0 || c->n_steps > (1 << 20)) return set_error(SNN_EINVAL, "n_steps out of range");
+    if (c->desired_period < 0) return set_error(SNN_EINVAL, "desired_period must be >= 0");
+    if (!(c->dt > 0)) return set_error(SNN_EINVAL, "dt must be positive");
+    return SNN_OK;
+}
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// ---- inference workspace: [n][22][N][10] f64 partials | [n] i32 arrivals
+size_t infer_ws(const snn_consts_t *c, int64_t n) {
+    return al((size_t)n * kMaxTiles * c->n_steps * kNO * sizeof(double)) + al((size_t)n * sizeof(int));
+}
+
+// ---- training workspace (per chunk)
+int64_t train_evcap(const snn_consts_t *c) {
+    // worst case: every hidden neuron fires as often as its refractory period allows
+    const int gap = std::max(1, (int)floor(c->lif_hid.refr));
+    const int64_t per_neuron = std::min<int64_t>(c->n_steps, c->n_steps / gap + 1);
+    return (int64_t)kNH * per_neuron;
+}
+
+size_t train_ws_per_image(const snn_consts_t *c) {
+    const size_t N = c->n_steps, cap = train_evcap(c);
+    return kMaxTiles * N * kTile * 2 + kMaxTiles * kTile * 2 + 4 + 4 + kNH * 2 + (kNH + 1) * 4 + cap * 2 +
+           (N + 1) * 4 + cap * 2 + N * 8 + kMaxTiles * N * 8;
+}
+
+int64_t train_chunk(const snn_consts_t *c, int64_t n) {
+    const size_t budget = (size_t)768 << 20;
+    int64_t ch = (int64_t)(budget / train_ws_per_image(c));
+    ch = std::max<int64_t>(1, std::min<int64_t>(ch, 1024));
+    return std::min<int64_t>(ch, std::max<int64_t>(n, 1));
+}
+
+size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base) {
+    const size_t N = c->n_steps, cap = train_evcap(c), n = chunk;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        char *p = base ? base + off : nullptr;
+        off += al(bytes);
+        return p;
+    };
+    TrainWS w;
+    w.raster = (uint16_t *)take(n * kMaxTiles * N * kTile * 2);
+    w.tile_pos = (uint16_t *)take(n * kMaxTiles * kTile * 2);
+    w.n_tiles = (int32_t *)take(n * 4);
+    w.n_act = (int32_t *)take(n * 4);
+    w.act_k = (uint16_t *)take(n * kNH * 2);
+    w.act_off = (int32_t *)take(n * (kNH + 1) * 4);
+    w.nsp = (uint16_t *)take(n * cap * 2);
+    w.step_off = (int32_t *)take(n * (N + 1) * 4);
+    w.step_k = (uint16_t *)take(n * cap * 2);
+    w.norm = (double *)take(n * N * 8);
+    w.wp = (double *)take(n * kMaxTiles * N * 8);
+    w.evcap = (int64_t)cap;
+    if (out) *out = w;
+    return off;
+}
+
+size_t train_smem(const snn_consts_t *c) { return ((size_t)c->n_steps * (2 * kNO + 1)) * sizeof(double); }
+
+}  // namespace
+
+extern "C" int snn_abi_version(void) { return SNN_ABI_VERSION; }
+extern "C" const char *snn_last_error(void) { return g_err; }
+
+extern "C" int snn_input_table(const snn_consts_t *c, double *d_ctab, uint8_t *d_spk, void *stream) {
+    int rc = validate(c);
+    if (rc) return rc;
+    if (!d_ctab) return set_error(SNN_EINVAL, "d_ctab is NULL");
+    k_input_table<<<1, 256, 0, (cudaStream_t)stream>>>(*c, d_ctab, d_spk);
+    return cuda_check("k_input_table");
+}
+
+extern "C" size_t snn_infer_workspace(const snn_consts_t *c, int64_t n) {
+    if (!c || n < 0 || c->n_steps <= 0) return 0;
+    return infer_ws(c, n);
+}
+
+extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t n, const double *d_w,
+                         const double *d_ctab, const snn_infer_out_t *out, void *d_ws, size_t ws_bytes,
+                         void *stream) {
+    int rc = validate(c);
+    if (rc) return rc;
+    if (n < 0) return set_error(SNN_EINVAL, "n_images < 0");
+    if (n == 0) return SNN_OK;
+    if (!out || !out->counts) return set_error(SNN_EINVAL, "counts output is required");
+    if (!d_images || !d_w || !d_ctab) return set_error(SNN_EINVAL, "NULL input pointer");
+    if (((uintptr_t)d_images & 15) != 0) return set_error(SNN_EINVAL, "images must be 16-byte aligned");
+    if (n * kGroups > 0x7fffffffLL) return set_error(SNN_EINVAL, "too many images in one call");
+    if (out->raster && (!out->tile_pos || !out->n_tiles))
+        return set_error(SNN_EINVAL, "raster output needs tile_pos and n_tiles");
+    if (!d_ws || ws_bytes < infer_ws(c, n)) return set_error(SNN_ENOMEM, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    HiddenArgs A;
+    memset(&A, 0, sizeof(A));
+    A.c = *c;
+    A.images = d_images;
+    A.n_images = n;
+    A.w = d_w;
+    A.ctab = d_ctab;
+    A.partial = (double *)d_ws;
+    A.arrive = (int *)((char *)d_ws + al((size_t)n * kMaxTiles * c->n_steps * kNO * sizeof(double)));
+    A.out = *out;
+    cudaMemsetAsync(A.arrive, 0, (size_t)n * sizeof(int), s);
+    const dim3 grid((unsigned)(n * kGroups));
+    const bool raster = out->raster != nullptr, trace = out->v_hid != nullptr;
+    if (raster && trace) k_hidden<true, true, true><<<grid, kThreads, 0, s>>>(A);
+    else if (raster) k_hidden<true, true, false><<<grid, kThreads, 0, s>>>(A);
+    else if (trace) k_hidden<true, false, true><<<grid, kThreads, 0, s>>>(A);
+    else k_hidden<true, false, false><<<grid, kThreads, 0, s>>>(A);
+    return cuda_check("k_hidden");
+}
+
+extern "C" size_t snn_train_workspace(const snn_consts_t *c, int64_t n) {
+    if (!c || n < 0 || c->n_steps <= 0) return 0;
+    return train_ws(c, train_chunk(c, n), nullptr, nullptr);
+}
+
+extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const uint8_t *d_labels, int64_t n,
+                         double *d_w, const double *d_ctab, int32_t *d_counts, int32_t *d_status, void *d_ws,
+                         size_t ws_bytes, void *stream) {
+    int rc = validate(c);
+    if (rc) return rc;
+    if (n < 0) return set_error(SNN_EINVAL, "n_images < 0");
+    if (!d_status) return set_error(SNN_EINVAL, "d_status is NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(d_status, 0, 4 * sizeof(int32_t), s);
+    if (n == 0) return cuda_check("snn_train");
+    if (!d_images || !d_labels || !d_w || !d_ctab || !d_counts) return set_error(SNN_EINVAL, "NULL pointer");
+    if (((uintptr_t)d_images & 15) != 0) return set_error(SNN_EINVAL, "images must be 16-byte aligned");
+    if (c->n_steps > 65535) return set_error(SNN_EINVAL, "training supports n_steps <= 65535");
+    const size_t smem = train_smem(c);
+    if (smem > 220 * 1024) return set_error(SNN_EINVAL, "n_steps too large for the sequential NormAD CTA");
+    const int64_t chunk = train_chunk(c, n);
+    TrainArgs T;
+    memset(&T, 0, sizeof(T));
+    const size_t need = train_ws(c, chunk, &T.ws, (char *)d_ws);
+    if (!d_ws || ws_bytes < need) return set_error(SNN_ENOMEM, "workspace too small");
+    if (cudaFuncSetAttribute(k_normad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return cuda_check("cudaFuncSetAttribute(k_normad)");
+    T.c = *c;
+    T.w = d_w;
+    T.status = d_status;
+    for (int64_t i0 = 0; i0 < n; i0 += chunk) {
+        const int64_t cn = std::min(chunk, n - i0);
+        HiddenArgs A;
+        memset(&A, 0, sizeof(A));
+        A.c = *c;
+        A.images = d_images + i0 * SNN_N_PIXELS;
+        A.n_images = cn;
+        A.w = d_w;
+        A.ctab = d_ctab;
+        A.out.raster = T.ws.raster;
+        A.out.tile_pos = T.ws.tile_pos;
+        A.out.n_tiles = T.ws.n_tiles;
+        k_hidden<false, true, false><<<(unsigned)(cn * kGroups), kThreads, 0, s>>>(A);
+        if ((rc = cuda_check("k_hidden<raster>"))) return rc;
+        T.n = cn;
+        T.first = i0;
+        T.labels = d_labels + i0;
+        T.counts = d_counts + i0 * kNO;
+        k_compact<<<(unsigned)cn, kCThreads, 0, s>>>(T);
+        if ((rc = cuda_check("k_compact"))) return rc;
+        k_normad<<<1, kTThreads, smem, s>>>(T);
+        if ((rc = cuda_check("k_normad"))) return rc;
+    }
+    return SNN_OK;
+}

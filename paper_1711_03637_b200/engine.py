@@ -1,0 +1,185 @@
+"""Device engine: constants, cached input tables, workspaces, stream, lock.
+
+One Engine per CUDA device.  All kernels run on the engine's own stream
+through the C ABI (``_native``); torch is used only for device memory and
+host<->device copies.  Calls are serialised by a lock, so the FastAPI
+thread-pool callers of ``run_presentation`` (service.py:107) are safe.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import threading
+
+import numpy as np
+
+from . import _native
+from .params import N_HIDDEN, N_INPUTS, N_OUTPUTS, TAU_LEARN, TAU_SYN_FAST, TAU_SYN_SLOW, desired_period
+
+_ENGINES: dict = {}
+_ENGINES_LOCK = threading.Lock()
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _lif(p, dt: float) -> _native.LifC:
+    """neurons.py:109-118, same float expression order as the reference."""
+    g, cap = float(p.leak_conductance), float(p.capacitance)
+    beta = dt * (2.0 - g * dt / cap) / (2.0 * cap)
+    return _native.LifC(g, float(p.rest_potential), float(p.threshold), beta, float(p.refractory) / dt)
+
+
+def make_consts(cfg, filters, learn=None) -> _native.ConstsC:
+    """Flatten NetworkConfig/FilterBank/LearnConfig (reference or mirror objects)."""
+    dt = float(cfg.dt)
+    c = _native.ConstsC()
+    c.n_steps = int(round(float(cfg.t) / dt))
+    c.desired_period = desired_period(float(cfg.t), dt, float(cfg.desired_rate))
+    c.dt = dt
+    c.i0 = float(cfg.encoding.i_0)
+    c.ip = float(cfg.encoding.i_p)
+    c.lif_in = _lif(cfg.input_lif, dt)
+    c.lif_hid = _lif(cfg.hidden_lif, dt)
+    c.lif_out = _lif(cfg.output_lif, dt)
+    c.decay_slow = math.exp(-dt / TAU_SYN_SLOW)      # neurons.py:148-150
+    c.decay_fast = math.exp(-dt / TAU_SYN_FAST)
+    c.decay_learn = math.exp(-dt / TAU_LEARN)        # normad.py:82
+    c.dhat_scale = dt / float(cfg.output_lif.capacitance)   # normad.py:83
+    c.inhibition = float(cfg.inhibition_weight)
+    if learn is not None:
+        c.learning_rate = float(learn.learning_rate)
+        c.norm_eps = float(learn.norm_epsilon)
+    taps = np.ascontiguousarray(np.asarray(filters.weighted, dtype=np.float64).reshape(12, 9))
+    ctypes.memmove(ctypes.addressof(c.taps), taps.ctypes.data, taps.nbytes)
+    # network.py:284-285 raises on non-finite hidden currents.  |c_in| <= 1/(1-decay_slow),
+    # so finite currents are guaranteed unless the gains are astronomically large.
+    bound = 9.0 * float(np.max(np.abs(taps))) / (1.0 - c.decay_slow)
+    if not (bound < 1e300):
+        raise ValueError("hidden currents contain non-finite values")
+    return c
+
+
+def table_key(c: _native.ConstsC):
+    li = c.lif_in
+    return (c.n_steps, c.dt, c.i0, c.ip, li.g, li.el, li.vt, li.beta, li.refr, c.decay_slow, c.decay_fast)
+
+
+class Engine:
+    def __init__(self, device=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1711_03637_b200 needs a CUDA device (no CPU fallback)")
+        self.lib = _native.load()
+        self.device = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+        with torch.cuda.device(self.device):
+            self.stream = torch.cuda.Stream(self.device)
+        self.lock = threading.RLock()
+        self._tables: dict = {}
+        self._ws: dict = {}
+
+    # ------------------------------------------------------------ helpers
+    @property
+    def sptr(self):
+        return ctypes.c_void_p(self.stream.cuda_stream)
+
+    def buffer(self, name: str, nbytes: int):
+        """Grow-only scratch buffer (uint8 tensor) on this device."""
+        torch = _torch()
+        buf = self._ws.get(name)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self._ws[name] = buf
+        return buf
+
+    def table(self, c: _native.ConstsC):
+        """(c_table [N,256] f64, spike table [N,256] u8) on device, cached per config."""
+        torch = _torch()
+        key = table_key(c)
+        hit = self._tables.get(key)
+        if hit is None:
+            with torch.cuda.stream(self.stream):
+                ctab = torch.empty((c.n_steps, 256), dtype=torch.float64, device=self.device)
+                spk = torch.empty((c.n_steps, 256), dtype=torch.uint8, device=self.device)
+            _native.check(self.lib.snn_input_table(ctypes.byref(c), ctab.data_ptr(), spk.data_ptr(), self.sptr))
+            torch.cuda.current_stream(self.device).wait_stream(self.stream)
+            if len(self._tables) >= 8:
+                self._tables.pop(next(iter(self._tables)))
+            hit = self._tables[key] = (ctab, spk)
+        return hit
+
+    # ------------------------------------------------------------ inference
+    def infer(self, c, images, w, *, raster=False, trace=False, max_chunk=None):
+        """Run n presentations.  images: uint8 [n,784] device tensor; w: f64
+        [8112,10] device tensor.  Returns dict of device tensors (counts int32
+        [n,10]; optionally raster/tile_pos/n_tiles/out_raster, ff/v_out/v_hid)."""
+        torch = _torch()
+        n = int(images.shape[0])
+        N = c.n_steps
+        ctab, _ = self.table(c)
+        dev = self.device
+        self.stream.wait_stream(torch.cuda.current_stream(dev))   # inputs made on the caller's stream
+        with torch.cuda.stream(self.stream):
+            out = {"counts": torch.empty((n, N_OUTPUTS), dtype=torch.int32, device=dev)}
+            if raster:
+                out["raster"] = torch.empty((n, _native.MAX_TILES, N, _native.TILE), dtype=torch.int16, device=dev)
+                out["tile_pos"] = torch.empty((n, _native.MAX_TILES, _native.TILE), dtype=torch.int16, device=dev)
+                out["n_tiles"] = torch.empty((n,), dtype=torch.int32, device=dev)
+                out["out_raster"] = torch.empty((n, N), dtype=torch.int16, device=dev)
+            if trace:
+                out["ff"] = torch.empty((n, N, N_OUTPUTS), dtype=torch.float64, device=dev)
+                out["v_out"] = torch.empty((n, N, N_OUTPUTS), dtype=torch.float64, device=dev)
+                out["v_hid"] = torch.full((n, N, N_HIDDEN), float(c.lif_hid.el), dtype=torch.float64, device=dev)
+        per_img = max(1, self.lib.snn_infer_workspace(ctypes.byref(c), 1))
+        chunk = max(1, min(n, (1 << 30) // per_img))
+        if max_chunk:
+            chunk = min(chunk, max_chunk)
+        assert images.dtype == torch.uint8 and images.is_contiguous() and images.shape[1] == N_INPUTS
+        assert w.dtype == torch.float64 and w.is_contiguous() and tuple(w.shape) == (N_HIDDEN, N_OUTPUTS)
+        for i0 in range(0, n, chunk):
+            cn = min(chunk, n - i0)
+            ws_bytes = self.lib.snn_infer_workspace(ctypes.byref(c), cn)
+            ws = self.buffer("infer", ws_bytes)
+            o = _native.InferOutC()
+            for name, t in out.items():
+                setattr(o, name, t[i0:i0 + cn].data_ptr())
+            _native.check(self.lib.snn_infer(
+                ctypes.byref(c), images[i0:i0 + cn].data_ptr(), cn, w.data_ptr(), ctab.data_ptr(),
+                ctypes.byref(o), ws.data_ptr(), ws_bytes, self.sptr))
+        torch.cuda.current_stream(dev).wait_stream(self.stream)   # results safe on the caller's stream
+        return out
+
+    # ------------------------------------------------------------ training
+    def train(self, c, images, labels, w):
+        """Sequential NormAD over n images (device tensors), updating w in place.
+        Returns (counts int32 [n,10] device, status int32 [4] device)."""
+        torch = _torch()
+        n = int(images.shape[0])
+        ctab, _ = self.table(c)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(self.stream):
+            counts = torch.zeros((n, N_OUTPUTS), dtype=torch.int32, device=self.device)
+            status = torch.zeros((4,), dtype=torch.int32, device=self.device)
+        ws_bytes = self.lib.snn_train_workspace(ctypes.byref(c), n)
+        ws = self.buffer("train", ws_bytes)
+        _native.check(self.lib.snn_train(
+            ctypes.byref(c), images.data_ptr(), labels.data_ptr(), n, w.data_ptr(), ctab.data_ptr(),
+            counts.data_ptr(), status.data_ptr(), ws.data_ptr(), ws_bytes, self.sptr))
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
+        return counts, status
+
+
+def get_engine(device=None) -> Engine:
+    torch = _torch()
+    if device is None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1711_03637_b200 needs a CUDA device (no CPU fallback)")
+        device = torch.cuda.current_device()
+    key = str(torch.device(device) if not isinstance(device, int) else torch.device("cuda", device))
+    with _ENGINES_LOCK:
+        eng = _ENGINES.get(key)
+        if eng is None:
+            eng = _ENGINES[key] = Engine(key)
+        return eng

@@ -1,0 +1,49 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GOLD = os.path.join(ROOT, "tests", "golden", "reference_golden.npz")
+DATA = os.path.join(ROOT, "data")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (run on the B200 box)")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+@pytest.fixture(scope="session")
+def golden():
+    return dict(np.load(GOLD))
+
+
+@pytest.fixture(scope="session")
+def workloads():
+    return dict(np.load(os.path.join(DATA, "workloads.npz")))
+
+
+@pytest.fixture(scope="session")
+def wfix():
+    return dict(np.load(os.path.join(DATA, "w_fix.npz")))
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    from oracle import snn_oracle
+    return snn_oracle
+
+
+@pytest.fixture(scope="session")
+def oparams(oracle):
+    return oracle.Params()
+
+
+@pytest.fixture(scope="session")
+def sd():
+    import paper_1711_03637_b200 as sd
+    return sd
