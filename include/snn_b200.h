@@ -76,17 +76,23 @@ typedef struct snn_consts {
     double taps[12][9];     /* FilterBank.weighted[f].ravel() (filters.py:57-60) */
 } snn_consts_t;
 
-/* Optional outputs of snn_infer; every pointer may be NULL except counts. */
+/* Optional outputs of snn_infer; every pointer may be NULL except counts.
+ * The hidden spike raster is compact: image i owns the block that starts at
+ * byte tile_base[i] * N * 64 and is laid out [step][tile][half][lane]; each
+ * byte is the 6-bit spike mask of features half*6 .. half*6+5 of the lane's
+ * window (tile_pos).  A raster buffer must hold n * 22 * N * 64 bytes (the
+ * upper bound). */
 typedef struct snn_infer_out {
     int32_t *counts;     /* [n][10] output spike counts */
-    uint16_t *raster;    /* [n][22][N][32] per-lane 12-bit hidden spike masks */
+    uint8_t *raster;     /* compact hidden raster (see above) */
     uint16_t *tile_pos;  /* [n][22][32] window position of each lane (0xFFFF = none) */
-    int32_t *n_tiles;    /* [n] live tiles per image */
+    int32_t *n_tiles;    /* [n] tiles (32 active windows each) per image */
+    int32_t *tile_base;  /* [n+1] exclusive prefix sum of n_tiles */
     uint16_t *out_raster;/* [n][N] 10-bit output spike masks */
     double *ff;          /* [n][N][10] feed-forward current c_hidden @ W */
     double *v_out;       /* [n][N][10] output membrane after each step */
     double *v_hid;       /* [n][N][8112] hidden membrane after each step (only
-                            neurons of live windows are written) */
+                            neurons of active windows are written) */
 } snn_infer_out_t;
 
 int snn_abi_version(void);

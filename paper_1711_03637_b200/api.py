@@ -60,18 +60,22 @@ def _fetch(eng, t) -> np.ndarray:
     return t.cpu().numpy()
 
 
-def decode_hidden(raster: np.ndarray, tile_pos: np.ndarray, n_tiles: int, n_steps: int) -> np.ndarray:
-    """Per-lane 12-bit masks -> (N, 8112) bool hidden spike raster of one image."""
+def decode_hidden(raster: np.ndarray, tile_base: int, tile_pos: np.ndarray, n_tiles: int,
+                  n_steps: int) -> np.ndarray:
+    """Compact raster block of one image -> (N, 8112) bool hidden spike raster.
+    Layout (include/snn_b200.h): bytes [tile_base*N*64 ...), [step][tile][half][lane],
+    6-bit masks of features half*6 .. half*6+5 of the lane's window."""
     out = np.zeros((n_steps, N_HIDDEN), dtype=bool)
     if n_tiles == 0:
         return out
+    blk = raster[tile_base * n_steps * 64:(tile_base + n_tiles) * n_steps * 64]
+    blk = blk.reshape(n_steps, n_tiles, 2, 32).astype(np.int64)
+    masks = blk[:, :, 0, :] | (blk[:, :, 1, :] << 6)              # (N, t, 32) 12-bit
     pos = tile_pos[:n_tiles].astype(np.int64) & 0xFFFF            # (t, 32)
-    masks = raster[:n_tiles].astype(np.int64) & 0xFFFF             # (t, N, 32)
     valid = pos != 0xFFFF
-    bits = (masks[..., None] >> np.arange(12)) & 1                 # (t, N, 32, 12)
+    bits = (masks[..., None] >> np.arange(12)) & 1                 # (N, t, 32, 12)
     idx = pos[:, :, None] * 12 + np.arange(12)                     # (t, 32, 12)
-    b = bits.transpose(1, 0, 2, 3)[:, valid]                       # (N, v, 12)
-    out[:, idx[valid].ravel()] = b.reshape(n_steps, -1).astype(bool)
+    out[:, idx[valid].ravel()] = bits[:, valid].reshape(n_steps, -1).astype(bool)
     return out
 
 
@@ -104,12 +108,13 @@ def run_presentation(image, weights, filters, cfg,
         out = eng.infer(c, d_img, d_w, raster=record)
         counts = _fetch(eng, out["counts"])[0].astype(np.int64)
         if record:
-            raster = out["raster"][0].cpu().numpy()
+            raster = out["raster"].cpu().numpy()
             tpos = out["tile_pos"][0].cpu().numpy()
             nt = int(out["n_tiles"][0].item())
+            tb = int(out["tile_base"][0].item())
             orast = out["out_raster"][0].cpu().numpy().astype(np.int64) & 0x3FF
     if record:
-        hidden = decode_hidden(raster, tpos, nt, c.n_steps)
+        hidden = decode_hidden(raster, tb, tpos, nt, c.n_steps)
         out_mask = ((orast[:, None] >> np.arange(N_OUTPUTS)) & 1).astype(bool)
         if _record_into is not None:
             _record_into["hidden_mask"] = hidden

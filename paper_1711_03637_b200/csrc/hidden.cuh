@@ -1,49 +1,68 @@
-// Inference hot path: input table, fused stencil + hidden LIF + event-driven
-// classifier contraction, and the 10-neuron output layer.  sm_100a.
+// Inference hot path on sm_100a: input table, window compaction, the fused
+// stencil + hidden-LIF kernel, and the event-driven output layer.
 //
 // Reference behaviour (relative to /root/reference/pkg/src/spikedigits):
 //   _input_tables          network.py:224-245  -> k_input_table
 //   hidden_current_series  network.py:254-264  -> stencil inside k_hidden
-//   run_presentation       network.py:267-326  -> k_hidden (+ scan_step)
+//   run_presentation       network.py:267-326  -> k_hidden + k_output
 //   lif_step / kernel_step neurons.py:83-171   -> snn_common.cuh helpers
 //
 // Work decomposition:
-//   * a "tile" is 32 consecutive ACTIVE window positions of one image (a
-//     window is active when any of its 9 pixels is non-zero; inactive windows
-//     receive exactly zero current and never leave rest, so skipping them is
-//     exact).  One warp owns one tile; each lane owns one window position and
-//     its 12 feature neurons, keeping v and the refractory horizon in
-//     registers for the whole trial.
-//   * the per-step input traces come from the 256-level table, staged 8 steps
-//     at a time into shared memory; the 3x3 stencil is the k-ordered FMA
-//     chain OpenBLAS uses for np.tensordot, so currents are bit-identical.
-//   * c_hidden @ W is computed event-driven: every hidden kernel trace is a
-//     linear recursion in its own spikes, so sum_k c_k(n) W[k,l] =
-//     A_l(n) - B_l(n) with A_l(n) = A_l(n-1)*e^{-dt/t1} + G_l(n), where G_l(n)
-//     is the sum of the W rows of the neurons spiking at step n.  Each warp
-//     writes its G partial per step; the last warp of an image to finish
-//     (atomic arrival counter) reduces the partials in fixed tile order and
-//     runs the sequential output layer.  Every reduction has a fixed order, so
-//     results are deterministic run to run.
+//   k_prep       a window (3x3 pixel patch, 676 per image) is ACTIVE when any
+//                of its pixels is non-zero.  Inactive windows receive exactly
+//                zero current for the whole trial and never leave rest, so
+//                skipping them is exact.  Active windows are compacted in
+//                ascending order into tiles of 32 (tile_pos), n_tiles per image.
+//   k_tile_scan  exclusive prefix of n_tiles -> tile_base: one compact list of
+//                all tiles of the batch, so no warp idles.
+//   k_hidden     persistent CTAs of 4 warps; a warp owns one tile, a lane one
+//                window and its 12 feature neurons (v, refractory horizon in
+//                registers for the whole trial).  The input-trace table is
+//                streamed through a 2-stage shared-memory ring by TMA bulk
+//                copies.  The stencil is the k-ordered FMA chain OpenBLAS uses
+//                for np.tensordot, so currents are bit-identical.  Output: one
+//                12-bit spike mask per lane and step (the raster).
+//   k_output     one warp per image.  c_hidden @ W is event-driven: every
+//                hidden kernel trace is a linear recursion in its own spikes,
+//                so sum_k c_k(n) W[k,l] = A_l(n) - B_l(n) with
+//                A_l(n) = A_l(n-1) e^{-dt/t1} + G_l(n), G_l(n) = sum of the W
+//                rows of the neurons spiking at n.  The warp gathers those W
+//                rows with cp.async (a whole batch in flight), sums them in
+//                ascending neuron order and runs the 10-neuron output layer.
+// Every reduction has a fixed order: results are deterministic run to run.
 #pragma once
 #include "snn_common.cuh"
 
 namespace snn {
 
-constexpr int kWPC = 4;                                // warps (tiles) per CTA
+constexpr int kWPC = 4;          // warps (tiles) per k_hidden CTA
 constexpr int kThreads = kWPC * 32;
-constexpr int kChunk = 8;                              // table steps per smem stage
-constexpr int kGroups = (kMaxTiles + kWPC - 1) / kWPC; // CTAs per image
+constexpr int kChunk = 8;        // table steps per ring stage
+constexpr int kStages = 2;       // table ring depth
+constexpr int kOutWarps = 4;     // images per k_output CTA (one warp each)
+constexpr int kOChunk = 4;       // steps per k_output pass
+constexpr int kEntCap = 64;      // spike entries per W-gather batch
 
-struct HiddenArgs {
+constexpr int kHalf = kNF / 2;   // features per k_hidden work item
+
+// Raster layout (bytes): image i owns the block starting at tile_base[i]*N*64,
+// laid out [step][tile][half][lane]; each byte is the 6-bit spike mask of
+// features half*6 .. half*6+5 of the lane's window.
+__host__ __device__ inline size_t raster_at(int64_t tile_base_img, int N, int ntiles, int s, int t) {
+    return ((size_t)tile_base_img * N + (size_t)s * ntiles + t) * (2 * kTile);
+}
+
+struct BatchArgs {
     snn_consts_t c;
-    const uint8_t *images;
+    const uint8_t *images;   // [n][784]
     int64_t n_images;
-    const double *w;
-    const double *ctab;
-    double *partial;   // [n][22][N][10] per-tile G partials (GSUM)
-    int *arrive;       // [n] arrival counters (zero on entry, reset on exit)
-    snn_infer_out_t out;
+    const double *w;         // [8112][10]
+    const double *ctab;      // [N][256]
+    uint16_t *tile_pos;      // [n][22][32] window of each lane, 0xFFFF = none
+    int32_t *n_tiles;        // [n]
+    int32_t *tile_base;      // [n+1] exclusive prefix of n_tiles
+    uint8_t *raster;         // sum(n_tiles) * N * 64 spike-mask bytes (see raster_at)
+    snn_infer_out_t out;     // counts / out_raster / ff / v_out / v_hid
 };
 
 // ---------------------------------------------------------------------------
@@ -68,10 +87,16 @@ __global__ void __launch_bounds__(256) k_input_table(snn_consts_t c, double *cta
 }
 
 // ---------------------------------------------------------------------------
-// Ordered compaction of the active window positions of one image (CTA-wide).
-__device__ __forceinline__ int compact_windows(const uint8_t *s_img, uint16_t *s_pos, int *s_cnt) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// k_prep: ordered compaction of the active windows, one image per CTA.
+__global__ void __launch_bounds__(kThreads) k_prep(const BatchArgs A) {
+    __shared__ __align__(16) uint8_t s_img[kSide * kSide];
+    __shared__ int s_cnt[8 * kWPC];
     constexpr int kIters = (kNPos + kThreads - 1) / kThreads;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t img = blockIdx.x;
+    const uint8_t *gimg = A.images + img * (kSide * kSide);
+    if (tid < 49) reinterpret_cast<uint4 *>(s_img)[tid] = __ldg(reinterpret_cast<const uint4 *>(gimg) + tid);
+    __syncthreads();
     unsigned bal[kIters];
 #pragma unroll
     for (int it = 0; it < kIters; ++it) {
@@ -96,12 +121,248 @@ __device__ __forceinline__ int compact_windows(const uint8_t *s_img, uint16_t *s
             if (w == warp) off[it] = run;
             run += s_cnt[it * kWPC + w];
         }
+    uint16_t *tp = A.tile_pos + img * (kMaxTiles * kTile);
+    for (int k = run + tid; k < kMaxTiles * kTile; k += kThreads) tp[k] = 0xFFFF;
 #pragma unroll
     for (int it = 0; it < kIters; ++it)
         if ((bal[it] >> lane) & 1u)
-            s_pos[off[it] + __popc(bal[it] & ((1u << lane) - 1u))] = (uint16_t)(it * kThreads + tid);
+            tp[off[it] + __popc(bal[it] & ((1u << lane) - 1u))] = (uint16_t)(it * kThreads + tid);
+    if (tid == 0) A.n_tiles[img] = (run + kTile - 1) / kTile;
+}
+
+// k_tile_scan: tile_base = exclusive prefix of n_tiles; one CTA, any n.
+__global__ void __launch_bounds__(1024) k_tile_scan(const BatchArgs A) {
+    __shared__ int s_w[32];
+    __shared__ int s_tot, s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry = 0;
     __syncthreads();
-    return run;
+    for (int64_t base = 0; base < A.n_images; base += 1024) {
+        const int64_t i = base + tid;
+        const int x = i < A.n_images ? A.n_tiles[i] : 0;
+        int tot;
+        const int ex = warp_excl_scan_int(x, &tot);
+        if (lane == 0) s_w[warp] = tot;
+        __syncthreads();
+        if (warp == 0) {
+            int t2;
+            const int e2 = warp_excl_scan_int(s_w[lane], &t2);
+            s_w[lane] = e2;
+            if (lane == 0) s_tot = t2;
+        }
+        __syncthreads();
+        if (i < A.n_images) A.tile_base[i] = s_carry + s_w[warp] + ex;
+        __syncthreads();
+        if (tid == 0) s_carry += s_tot;
+        __syncthreads();
+    }
+    if (tid == 0) A.tile_base[A.n_images] = s_carry;
+}
+
+// ---------------------------------------------------------------------------
+// The default filter bank (filters.py:22-31, :63-88) as compile-time taps:
+// kernels * (15 nA / positive sum), evaluated in IEEE double exactly like
+// numpy does on the host.  The library uses the specialised kernel only when
+// the caller's taps are bitwise identical to these.
+constexpr double kG1 = 15e-9 / 4.0;   // Sobel gain
+constexpr double kG2 = 15e-9 / 20.0;  // corner gain
+// integer kernel coefficients (filters.py:22-31, negations, corners)
+__host__ __device__ constexpr int def_coef(int f, int k) {
+    constexpr int c[kNF][9] = {
+        {1, 2, 1, 0, 0, 0, -1, -2, -1},    {1, 0, -1, 2, 0, -2, 1, 0, -1},
+        {2, 1, 0, 1, 0, -1, 0, -1, -2},    {0, 1, 2, -1, 0, 1, -2, -1, 0},
+        {-1, -2, -1, 0, 0, 0, 1, 2, 1},    {-1, 0, 1, -2, 0, 2, -1, 0, 1},
+        {-2, -1, 0, -1, 0, 1, 0, 1, 2},    {0, -1, -2, 1, 0, -1, 2, 1, 0},
+        {5, 5, -4, 5, 5, -4, -4, -4, -4},  {-4, 5, 5, -4, 5, 5, -4, -4, -4},
+        {-4, -4, -4, 5, 5, -4, 5, 5, -4},  {-4, -4, -4, -4, 5, 5, -4, 5, 5},
+    };
+    return c[f][k];
+}
+
+// FilterBank.weighted = kernels * gains[:, None, None] (float64 product)
+__host__ __device__ constexpr double def_tap(int f, int k) {
+    return (double)def_coef(f, k) * (f < 8 ? kG1 : kG2);
+}
+
+// dgemm's k-ordered FMA chain for a compile-time tap row.  A zero tap adds
+// x*0 = +0 (inputs are >= 0), which leaves the sum unchanged up to the sign
+// of a zero, so skipping it is exact for everything downstream.
+template <int F>
+__device__ __forceinline__ double def_current(const double (&x)[9]) {
+    double I = 0.0;
+    bool first = true;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        if (def_coef(F, k) != 0) {
+            I = first ? __dmul_rn(x[k], def_tap(F, k)) : __fma_rn(x[k], def_tap(F, k), I);
+            first = false;
+        }
+    }
+    return I;
+}
+
+__device__ __forceinline__ void lif_update(double I, double &v, int &live_from, int s, int relive,
+                                           const snn_lif_t &ph, unsigned &m, int bit) {
+    const double cand = lif_candidate(v, I, ph);
+    const bool ok = s >= live_from;
+    const bool fired = ok && cand >= ph.vt;
+    v = ok ? (fired ? ph.el : cand) : v;
+    live_from = fired ? relive : live_from;
+    m |= (fired ? 1u : 0u) << bit;
+}
+
+// All 12 features of one lane with the default bank: 4 Sobel currents, their
+// exact negations (fma(x,-w,-a) == -fma(x,w,a) under round-to-nearest-even),
+// and 4 corner currents -- 60 FMAs instead of 108.
+__device__ __forceinline__ unsigned hidden_step_def(const snn_lif_t &ph, const double (&x)[9],
+                                                    double (&v)[kNF], int (&live_from)[kNF], int s,
+                                                    int relive) {
+    unsigned m = 0;
+    const double e0 = def_current<0>(x), e1 = def_current<1>(x), e2 = def_current<2>(x), e3 = def_current<3>(x);
+    lif_update(e0, v[0], live_from[0], s, relive, ph, m, 0);
+    lif_update(e1, v[1], live_from[1], s, relive, ph, m, 1);
+    lif_update(e2, v[2], live_from[2], s, relive, ph, m, 2);
+    lif_update(e3, v[3], live_from[3], s, relive, ph, m, 3);
+    lif_update(-e0, v[4], live_from[4], s, relive, ph, m, 4);
+    lif_update(-e1, v[5], live_from[5], s, relive, ph, m, 5);
+    lif_update(-e2, v[6], live_from[6], s, relive, ph, m, 6);
+    lif_update(-e3, v[7], live_from[7], s, relive, ph, m, 7);
+    lif_update(def_current<8>(x), v[8], live_from[8], s, relive, ph, m, 8);
+    lif_update(def_current<9>(x), v[9], live_from[9], s, relive, ph, m, 9);
+    lif_update(def_current<10>(x), v[10], live_from[10], s, relive, ph, m, 10);
+    lif_update(def_current<11>(x), v[11], live_from[11], s, relive, ph, m, 11);
+    return m;
+}
+
+// Generic bank: one lane's 6 feature neurons (features H*6 .. H*6+5).
+template <int H>
+__device__ __forceinline__ unsigned hidden_step(const BatchArgs &A, const double (&x)[9], double (&v)[kNF],
+                                                int (&live_from)[kNF], int s, int relive) {
+    const snn_lif_t &ph = A.c.lif_hid;
+    double I[kHalf];
+#pragma unroll
+    for (int f = 0; f < kHalf; ++f) I[f] = __dmul_rn(x[0], A.c.taps[H * kHalf + f][0]);
+#pragma unroll
+    for (int k = 1; k < 9; ++k)
+#pragma unroll
+        for (int f = 0; f < kHalf; ++f) I[f] = __fma_rn(x[k], A.c.taps[H * kHalf + f][k], I[f]);
+    unsigned m = 0;
+#pragma unroll
+    for (int f = 0; f < kHalf; ++f) lif_update(I[f], v[f], live_from[f], s, relive, ph, m, f);
+    return m;
+}
+
+// k_hidden: persistent CTAs walk groups of kWPC consecutive work items.  With
+// the default bank (DEF) an item is a tile: a warp owns 32 windows x 12
+// features.  With a generic bank an item is (tile, half): 32 windows x 6
+// features, which keeps the 54 runtime taps of a warp within the register
+// budget.  The table chunks form one continuous stream across groups, so the
+// TMA ring never drains between groups.
+template <bool TRACE, bool DEF>
+__global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
+    __shared__ __align__(128) double s_tab[kStages][kChunk * 256];
+    __shared__ uint64_t s_full[kStages];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int N = A.c.n_steps;
+    const int nchunks = (N + kChunk - 1) / kChunk;
+    const int64_t n = A.n_images;
+    constexpr int kItemsPerTile = DEF ? 1 : 2;
+    const int total = kItemsPerTile * A.tile_base[n];
+    const int ngroups = (total + kWPC - 1) / kWPC;
+    if ((int)blockIdx.x >= ngroups) return;
+    const int my_groups = (ngroups - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int64_t stream_len = (int64_t)my_groups * nchunks;
+
+    auto issue = [&](int64_t q) {
+        const int ch = (int)(q % nchunks), b = (int)(q % kStages);
+        const int rows = min(kChunk, N - ch * kChunk);
+        mbar_expect_tx(&s_full[b], rows * 256 * 8);
+        bulk_g2s(s_tab[b], A.ctab + (size_t)ch * kChunk * 256, rows * 256 * 8, &s_full[b]);
+    };
+    if (tid == 0) {
+        for (int b = 0; b < kStages; ++b) mbar_init(&s_full[b], 1);
+        fence_mbar_init();
+        for (int64_t q = 0; q < kStages && q < stream_len; ++q) issue(q);
+    }
+    __syncthreads();
+
+    const double el = A.c.lif_hid.el, refr = A.c.lif_hid.refr;
+    int64_t q = 0;
+    for (int gi = 0; gi < my_groups; ++gi) {
+        const int item = ((int)blockIdx.x + gi * (int)gridDim.x) * kWPC + warp;
+        const bool live = item < total;  // warp-uniform
+        const int gt = DEF ? item : item >> 1, half = DEF ? 0 : item & 1;
+        int64_t img = 0;
+        int tile = 0, pos = 0, nt = 0;
+        if (live) {
+            int64_t lo = 0, hi = n - 1;  // last image with tile_base <= gt
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (A.tile_base[mid] <= gt) lo = mid;
+                else hi = mid - 1;
+            }
+            img = lo;
+            tile = gt - A.tile_base[img];
+            nt = A.n_tiles[img];
+            pos = A.tile_pos[img * (kMaxTiles * kTile) + tile * kTile + lane];
+        }
+        const bool on = live && pos != 0xFFFF;
+        uint32_t lvp[3];  // the 9 pixel levels of this lane's window, 4 per word
+        {
+            const int p = on ? pos : 0;
+            const int r = p / kFmap, col = p % kFmap;
+            const uint8_t *im = A.images + img * (kSide * kSide);
+            lvp[0] = lvp[1] = lvp[2] = 0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                    const int k = a * 3 + b;
+                    const uint32_t lev = on ? __ldg(im + (r + a) * kSide + col + b) : 0u;
+                    lvp[k >> 2] |= lev << (8 * (k & 3));
+                }
+        }
+        double v[kNF];
+        int live_from[kNF];
+#pragma unroll
+        for (int f = 0; f < kNF; ++f) {
+            v[f] = el;
+            live_from[f] = 0;
+        }
+        uint8_t *rout = live ? A.raster + raster_at(A.tile_base[img], N, nt, 0, tile) + half * kTile + lane : nullptr;
+        const size_t rstride = (size_t)nt * 2 * kTile;
+
+        for (int ch = 0; ch < nchunks; ++ch, ++q) {
+            const int b = (int)(q % kStages);
+            const int s0 = ch * kChunk;
+            const int nrows = min(kChunk, N - s0);
+            if (live) {
+                mbar_wait(&s_full[b], (uint32_t)((q / kStages) & 1));
+#pragma unroll 1
+                for (int j = 0; j < nrows; ++j) {
+                    const int s = s0 + j;
+                    const double *T = s_tab[b] + j * 256;
+                    double x[9];
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) x[k] = T[(lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu];
+                    const int relive = next_live_step(s, refr);
+                    unsigned m;
+                    if (DEF) m = hidden_step_def(A.c.lif_hid, x, v, live_from, s, relive);
+                    else m = half ? hidden_step<1>(A, x, v, live_from, s, relive)
+                                  : hidden_step<0>(A, x, v, live_from, s, relive);
+                    if (TRACE && on && A.out.v_hid) {
+                        double *dst = A.out.v_hid + ((size_t)img * N + s) * kNH + pos * kNF + half * kHalf;
+#pragma unroll
+                        for (int f = 0; f < (DEF ? kNF : kHalf); ++f) dst[f] = v[f];
+                    }
+                    rout[(size_t)s * rstride] = (uint8_t)(m & 0x3Fu);
+                    if (DEF) rout[(size_t)s * rstride + kTile] = (uint8_t)(m >> kHalf);
+                }
+            }
+            __syncthreads();  // every warp is done with stage b
+            if (tid == 0 && q + kStages < stream_len) issue(q + kStages);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -150,34 +411,151 @@ __device__ __forceinline__ bool out_step(OutState &st, const snn_consts_t &c, do
     return fired;
 }
 
-// Inference output layer: G for 32 steps at a time reduced from the tile
-// partials in tile order into s_buf, then scanned.  One full warp.
-__device__ void infer_output_layer(const HiddenArgs &A, int64_t img, int ntiles, double *s_buf) {
+// ---------------------------------------------------------------------------
+// k_output: one warp per image -- G from the raster and W, then the output layer.
+struct OutSmem {
+    uint4 rast[kOChunk * kMaxTiles * kTile * 2 / 16];  // raster bytes of kOChunk steps
+    double gval[kEntCap * kNO];                        // gathered W rows of staged spikes
+    double G[kOChunk * kNO];
+    uint16_t pos[kMaxTiles * kTile];
+    uint16_t ent[kEntCap];                             // neuron ids, ascending within a step
+    uint8_t ent_j[kEntCap];                            // chunk-relative step of each entry
+};
+
+__device__ __forceinline__ uint64_t warp_excl_scan_u64(uint64_t x, uint64_t *total) {
     const int lane = threadIdx.x & 31;
+    uint64_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += y;
+    }
+    *total = __shfl_sync(kFull, inc, 31);
+    return inc - x;
+}
+
+__global__ void __launch_bounds__(kOutWarps * 32) k_output(const BatchArgs A) {
+    extern __shared__ __align__(16) uint8_t osmem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    OutSmem &S = reinterpret_cast<OutSmem *>(osmem)[warp];
+    const int64_t img = (int64_t)blockIdx.x * kOutWarps + warp;
+    if (img >= A.n_images) return;
     const int N = A.c.n_steps;
+    const int nt = A.n_tiles[img];
+    const int64_t tb = A.tile_base[img];
     const int l = lane < kNO ? lane : kNO - 1;
-    const double *P = A.partial + (size_t)img * kMaxTiles * N * kNO;
-    OutState st;
-    out_init(st, A.c);
-    for (int s0 = 0; s0 < N; s0 += 32) {
-        const int ns = min(32, N - s0);
-        if (lane < ns) {
-            double G[kNO];
-#pragma unroll
-            for (int k = 0; k < kNO; ++k) G[k] = 0.0;
-            for (int t = 0; t < ntiles; ++t) {
-                const double *src = P + ((size_t)t * N + s0 + lane) * kNO;
-#pragma unroll
-                for (int k = 0; k < kNO; ++k) G[k] = __dadd_rn(G[k], ldcg(src + k));
+    for (int k = lane; k < nt * kTile; k += 32) S.pos[k] = A.tile_pos[img * (kMaxTiles * kTile) + k];
+
+    int fill = 0;
+    // Gather the W rows of the staged spikes (5 x 16 B cp.async per row, all in
+    // flight at once), then add them to G in list order.  Lane l keeps the
+    // running sum of the current step in a register.
+    auto flush = [&]() {
+        __syncwarp();
+        for (int t = lane; t < fill * 5; t += 32) {
+            const int e = t / 5, part = t - e * 5;
+            cp_async16(&S.gval[e * kNO + part * 2], A.w + (size_t)S.ent[e] * kNO + part * 2);
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        if (lane < kNO && fill > 0) {
+            int cj = S.ent_j[0];
+            double g = S.G[cj * kNO + lane];
+            for (int e = 0; e < fill; ++e) {
+                const int j = S.ent_j[e];
+                if (j != cj) {
+                    S.G[cj * kNO + lane] = g;
+                    cj = j;
+                    g = S.G[j * kNO + lane];
+                }
+                g = __dadd_rn(g, S.gval[e * kNO + lane]);
             }
-#pragma unroll
-            for (int k = 0; k < kNO; ++k) s_buf[lane * kNO + k] = G[k];
+            S.G[cj * kNO + lane] = g;
         }
         __syncwarp();
+        fill = 0;
+    };
+    // Stage the spikes of `tot` entries with lane-local offsets `off`, in
+    // windows that fit the buffer (a burst larger than the buffer is split).
+    auto emit = [&](unsigned m, int off, int tot, int j, int id0) {
+        for (int done = 0; done < tot;) {
+            if (fill == kEntCap) flush();
+            const int take = min(kEntCap - fill, tot - done);
+            int r = 0;
+            unsigned mm = m;
+            while (mm) {
+                const int f = __ffs(mm) - 1;
+                mm &= mm - 1;
+                const int idx = off + r++ - done;
+                if (idx >= 0 && idx < take) {
+                    S.ent[fill + idx] = (uint16_t)(id0 + f);
+                    S.ent_j[fill + idx] = (uint8_t)j;
+                }
+            }
+            fill += take;
+            done += take;
+        }
+    };
+
+    OutState st;
+    out_init(st, A.c);
+    for (int s0 = 0; s0 < N; s0 += kOChunk) {
+        const int ns = min(kOChunk, N - s0);
+        {   // the raster of steps s0..s0+ns-1 is contiguous: ns * nt * 64 B
+            const uint4 *src = reinterpret_cast<const uint4 *>(A.raster + raster_at(tb, N, nt, s0, 0));
+            const int nvec = ns * nt * (kTile * 2 / 16);
+            for (int k = lane; k < nvec; k += 32) S.rast[k] = __ldcg(src + k);
+        }
+        for (int k = lane; k < ns * kNO; k += 32) S.G[k] = 0.0;
+        __syncwarp();
+        const uint8_t *rm = reinterpret_cast<const uint8_t *>(S.rast);
+        for (int j = 0; j < ns; ++j) {
+            for (int t0 = 0; t0 < nt; t0 += 4) {
+                // four tiles per packed 64-bit scan (16-bit counts, <= 384 each)
+                unsigned m[4];
+                uint64_t pk = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int t = t0 + q;
+                    m[q] = 0;
+                    if (t < nt) {
+                        const uint8_t *row = rm + (j * nt + t) * (2 * kTile);
+                        m[q] = (unsigned)row[lane] | ((unsigned)row[kTile + lane] << kHalf);
+                    }
+                    pk |= (uint64_t)__popc(m[q]) << (16 * q);
+                }
+                uint64_t tot4;
+                const uint64_t off4 = warp_excl_scan_u64(pk, &tot4);
+                if (tot4 == 0) continue;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int tot = (int)((tot4 >> (16 * q)) & 0xFFFF);
+                    if (tot == 0) continue;
+                    const int off = (int)((off4 >> (16 * q)) & 0xFFFF);
+                    if (fill + tot <= kEntCap) {
+                        if (m[q]) {
+                            int k = fill + off;
+                            const int id0 = S.pos[(t0 + q) * kTile + lane] * kNF;
+                            unsigned mm = m[q];
+                            while (mm) {
+                                const int f = __ffs(mm) - 1;
+                                mm &= mm - 1;
+                                S.ent[k] = (uint16_t)(id0 + f);
+                                S.ent_j[k++] = (uint8_t)j;
+                            }
+                        }
+                        fill += tot;
+                    } else {
+                        emit(m[q], off, tot, j, m[q] ? S.pos[(t0 + q) * kTile + lane] * kNF : 0);
+                    }
+                }
+            }
+        }
+        flush();
         for (int j = 0; j < ns; ++j) {
             const int s = s0 + j;
             double ff;
-            const bool fired = out_step(st, A.c, s_buf[j * kNO + l], s, &ff);
+            const bool fired = out_step(st, A.c, S.G[j * kNO + l], s, &ff);
             const unsigned om = __ballot_sync(kFull, fired) & 0x3FFu;
             if (A.out.out_raster && lane == 0) A.out.out_raster[(size_t)img * N + s] = (uint16_t)om;
             if (lane < kNO) {
@@ -190,137 +568,6 @@ __device__ void infer_output_layer(const HiddenArgs &A, int64_t img, int ntiles,
     if (lane < kNO) A.out.counts[(size_t)img * kNO + lane] = st.cnt;
 }
 
-// ---------------------------------------------------------------------------
-// The fused hidden-layer kernel.  grid = n_images * kGroups CTAs of kWPC warps.
-//   GSUM   : per-step G partials + last-arriver output layer (inference)
-//   RASTER : per-lane 12-bit spike masks per step (training / forward_pass)
-//   TRACE  : hidden membrane after every step (parity tests)
-template <bool GSUM, bool RASTER, bool TRACE>
-__global__ void __launch_bounds__(kThreads) k_hidden(const HiddenArgs A) {
-    __shared__ __align__(16) double s_tab[kChunk * 256];
-    __shared__ __align__(16) uint8_t s_img[kSide * kSide];
-    __shared__ uint16_t s_pos[kNPos + 4];
-    __shared__ int s_cnt[8 * kWPC];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t img = blockIdx.x / kGroups;
-    const int grp = blockIdx.x % kGroups;
-    const int N = A.c.n_steps;
-
-    // stage the image (784 B = 49 x 16 B)
-    const uint8_t *gimg = A.images + img * (kSide * kSide);
-    if (tid < 49) reinterpret_cast<uint4 *>(s_img)[tid] = __ldg(reinterpret_cast<const uint4 *>(gimg) + tid);
-    __syncthreads();
-    const int n_act = compact_windows(s_img, s_pos, s_cnt);
-    const int ntiles = (n_act + kTile - 1) / kTile;
-    if (RASTER && grp == 0 && tid == 0 && A.out.n_tiles) A.out.n_tiles[img] = ntiles;
-    if (ntiles == 0) {
-        // blank image: the hidden layer stays at rest and G == 0 every step
-        if (GSUM && grp == 0 && warp == 0) infer_output_layer(A, img, 0, s_tab);
-        return;
-    }
-    if (grp * kWPC >= ntiles) return;  // whole CTA beyond the image's tiles
-
-    const int tile = grp * kWPC + warp;
-    const bool live = tile < ntiles;  // warp-uniform
-    const int slot = tile * kTile + lane;
-    const bool on = live && slot < n_act;
-    const int pos = on ? s_pos[slot] : 0;
-    if (RASTER && live && A.out.tile_pos)
-        A.out.tile_pos[((size_t)img * kMaxTiles + tile) * kTile + lane] = on ? (uint16_t)pos : (uint16_t)0xFFFF;
-
-    // the 9 pixel levels of this lane's window = column offsets into a table row
-    int lv[9];
-    {
-        const int r = pos / kFmap, col = pos % kFmap;
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) lv[a * 3 + b] = on ? s_img[(r + a) * kSide + col + b] : 0;
-    }
-
-    const snn_lif_t &ph = A.c.lif_hid;
-    double v[kNF];
-    int live_from[kNF];
-#pragma unroll
-    for (int f = 0; f < kNF; ++f) {
-        v[f] = ph.el;
-        live_from[f] = 0;
-    }
-    double *Pt = GSUM ? A.partial + ((size_t)img * kMaxTiles + tile) * N * kNO : nullptr;
-    uint16_t *Rt = RASTER ? A.out.raster + ((size_t)img * kMaxTiles + tile) * N * kTile : nullptr;
-    const double *wbase = A.w + (lane < kNO ? lane : 0);
-
-    for (int s0 = 0; s0 < N; s0 += kChunk) {
-        const int nrows = min(kChunk, N - s0);
-        __syncthreads();
-        {
-            const double2 *src = reinterpret_cast<const double2 *>(A.ctab + (size_t)s0 * 256);
-            double2 *dst = reinterpret_cast<double2 *>(s_tab);
-            for (int i = tid; i < nrows * 128; i += kThreads) dst[i] = __ldg(src + i);
-        }
-        __syncthreads();
-        if (!live) continue;
-        for (int j = 0; j < nrows; ++j) {
-            const int s = s0 + j;
-            const double *T = s_tab + j * 256;
-            double x[9];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) x[k] = T[lv[k]];
-            const int relive = next_live_step(s, ph.refr);
-            unsigned m = 0;
-#pragma unroll
-            for (int f = 0; f < kNF; ++f) {
-                // network.py:220 -- dgemm's k-ordered FMA chain over the 9 taps
-                double I = __dmul_rn(x[0], A.c.taps[f][0]);
-#pragma unroll
-                for (int k = 1; k < 9; ++k) I = __fma_rn(x[k], A.c.taps[f][k], I);
-                const double cand = lif_candidate(v[f], I, ph);
-                const bool ok = s >= live_from[f];
-                const bool fired = ok && cand >= ph.vt;
-                v[f] = ok ? (fired ? ph.el : cand) : v[f];
-                live_from[f] = fired ? relive : live_from[f];
-                m |= (fired ? 1u : 0u) << f;
-            }
-            if (TRACE && on && A.out.v_hid) {
-                double *dst = A.out.v_hid + ((size_t)img * N + s) * kNH + pos * kNF;
-#pragma unroll
-                for (int f = 0; f < kNF; ++f) dst[f] = v[f];
-            }
-            if (RASTER) Rt[(size_t)s * kTile + lane] = (uint16_t)m;
-            if (GSUM) {
-                unsigned bal = __ballot_sync(kFull, m != 0);
-                double g = 0.0;
-                while (bal) {
-                    const int src = __ffs(bal) - 1;
-                    bal &= bal - 1;
-                    unsigned mm = __shfl_sync(kFull, m, src);
-                    const int pp = __shfl_sync(kFull, pos, src);
-                    const double *wr = wbase + (size_t)pp * (kNF * kNO);
-                    while (mm) {
-                        const int f = __ffs(mm) - 1;
-                        mm &= mm - 1;
-                        if (lane < kNO) g = __dadd_rn(g, __ldg(wr + f * kNO));
-                    }
-                }
-                if (lane < kNO) Pt[(size_t)s * kNO + lane] = g;
-            }
-        }
-    }
-    if (GSUM) {
-        __syncthreads();  // every warp of this CTA is done with s_tab
-        if (live) {
-            __threadfence();
-            int prev = 0;
-            if (lane == 0) prev = atomicAdd(A.arrive + img, 1);
-            prev = __shfl_sync(kFull, prev, 0);
-            if (prev == ntiles - 1) {
-                __threadfence();
-                infer_output_layer(A, img, ntiles, s_tab);
-                if (lane == 0) A.arrive[img] = 0;
-            }
-        }
-    }
-}
+constexpr size_t kOutSmemBytes = sizeof(OutSmem) * kOutWarps;
 
 }  // namespace snn

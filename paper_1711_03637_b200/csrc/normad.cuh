@@ -28,18 +28,19 @@
 namespace snn {
 
 constexpr int kCThreads = kMaxTiles * 32;  // 704: one thread per (tile, lane) slot
-constexpr int kTThreads = 1024;            // sequential NormAD CTA
+constexpr int kTThreads = 512;             // sequential NormAD CTA (128 regs/thread)
 
 struct TrainWS {
-    uint16_t *raster;   // [n][22][N][32]
+    uint8_t *raster;    // sum(n_tiles) x N x 64 bytes (raster_at layout)
     uint16_t *tile_pos; // [n][22][32]
     int32_t *n_tiles;   // [n]
+    int32_t *tile_base; // [n+1]
     int32_t *n_act;     // [n]
     uint16_t *act_k;    // [n][8112]  active neuron ids, ascending
     int32_t *act_off;   // [n][8113]  per active neuron: start in nsp
     uint16_t *nsp;      // [n][evcap] spike steps per active neuron
     int32_t *step_off;  // [n][N+1]   per step: start in step_k
-    uint16_t *step_k;   // [n][evcap] spiking neuron ids per step, ascending
+    uint16_t *step_k;   // [n][evcap] per step: active-list index of each spiking neuron, ascending
     double *norm;       // [n][N]     |d_hat(s)|
     double *wp;         // [n][22][N] per-warp partial sums of d_hat^2
     int64_t evcap;
@@ -100,7 +101,9 @@ __global__ void __launch_bounds__(kCThreads) k_compact(const TrainArgs T) {
     int pos = 0xFFFF;
     if (tile < ntiles) pos = W.tile_pos[((size_t)img * kMaxTiles + tile) * kTile + lane];
     const bool valid = pos != 0xFFFF;
-    const uint16_t *R = W.raster + ((size_t)img * kMaxTiles + tile) * N * kTile + lane;
+    const size_t rstride = (size_t)ntiles * 2 * kTile;  // raster step stride of this image
+    const uint8_t *R = W.raster + (tile < ntiles ? raster_at(W.tile_base[img], N, ntiles, 0, tile) : 0) + lane;
+    auto mask12 = [&](int s) { return (unsigned)R[(size_t)s * rstride] | ((unsigned)R[(size_t)s * rstride + kTile] << kHalf); };
 
     // pass 1: which of my 12 neurons ever fire, and how often
     unsigned ever = 0;
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(kCThreads) k_compact(const TrainArgs T) {
     for (int f = 0; f < kNF; ++f) cnt[f] = 0;
     if (valid)
         for (int s = 0; s < N; ++s) {
-            const unsigned m = R[(size_t)s * kTile];
+            const unsigned m = mask12(s);
             ever |= m;
 #pragma unroll
             for (int f = 0; f < kNF; ++f) cnt[f] += (m >> f) & 1u;
@@ -136,8 +139,9 @@ __global__ void __launch_bounds__(kCThreads) k_compact(const TrainArgs T) {
         act_off[n_act] = (int32_t)n_ev;
     }
     int cursor[kNF];
+    const int act_base = (int)(ex >> 40);
     {
-        int r = (int)(ex >> 40), e = (int)(ex & kLow);
+        int r = act_base, e = (int)(ex & kLow);
 #pragma unroll
         for (int f = 0; f < kNF; ++f) {
             cursor[f] = e;
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(kCThreads) k_compact(const TrainArgs T) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int s = s0 + q;
-            ms[q] = (valid && s < N) ? (unsigned)R[(size_t)s * kTile] : 0u;
+            ms[q] = (valid && s < N) ? mask12(s) : 0u;
             pk |= (uint64_t)__popc(ms[q]) << (16 * q);
         }
         uint64_t t4;
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(kCThreads) k_compact(const TrainArgs T) {
 #pragma unroll
                 for (int f = 0; f < kNF; ++f)
                     if ((m >> f) & 1u) {
-                        step_k[o++] = (uint16_t)(pos * kNF + f);
+                        step_k[o++] = (uint16_t)(act_base + __popc(ever & ((1u << f) - 1u)));
                         nsp[cursor[f]++] = (uint16_t)s;
                     }
             }
@@ -226,13 +230,45 @@ __global__ void __launch_bounds__(kCThreads) k_compact(const TrainArgs T) {
 
 // ---------------------------------------------------------------------------
 // K3: the sequential part, one CTA walking the chunk's images in order.
-// dynamic smem: GR[N*10] (G, then R) | SIG[N*10] | H[N] | flags
-__global__ void __launch_bounds__(kTThreads) k_normad(const TrainArgs T) {
+//
+// Per image everything the weight-dependent chain touches is staged in shared
+// memory first (step lists, spike lists, |d_hat|, and the W rows of the
+// image's active neurons, ~80 KB), so the chain itself runs out of smem:
+//   G -> output scan (one warp; the only serial part) -> R (adjoint, O(N))
+//   -> dW / W update of the active rows (all-or-nothing, normad.py:122-124).
+// Images whose lists do not fit the smem caps take the same path reading the
+// lists and W from global memory instead.
+struct NormadCaps {
+    int acap;   // active neurons whose W rows / lists fit in smem
+    int ecap;   // spike events whose lists fit in smem
+};
+
+__host__ __device__ inline size_t normad_smem_bytes(int N, NormadCaps cap) {
+    size_t b = 0;
+    b += (size_t)N * kNO * 8 * 2;            // GR, SIG
+    b += (size_t)N * 8 * 2;                  // H, NRM
+    b += (size_t)cap.acap * kNO * 8;         // WACT
+    b += ((size_t)N + 1) * 4;                // SOFF
+    b += ((size_t)cap.acap + 1) * 4;         // AOFF
+    b += (size_t)cap.acap * 2;               // AK
+    b += (size_t)cap.ecap * 2 * 2;           // EV, NSP
+    return b + 64;
+}
+
+__global__ void __launch_bounds__(kTThreads) k_normad(const TrainArgs T, const NormadCaps cap) {
     extern __shared__ __align__(16) double smem[];
     const int N = T.c.n_steps;
-    double *GR = smem;
-    double *SIG = GR + (size_t)N * kNO;
+    double *GR = smem;                             // G(s,l), then R(u,l)
+    double *SIG = GR + (size_t)N * kNO;            // sigma(s,l)
     double *H = SIG + (size_t)N * kNO;
+    double *NRM = H + N;
+    double *WACT = NRM + N;                        // [acap][10] W rows of active neurons
+    int *SOFF = reinterpret_cast<int *>(WACT + (size_t)cap.acap * kNO);
+    int *AOFF = SOFF + N + 1;
+    uint16_t *AK = reinterpret_cast<uint16_t *>(AOFF + cap.acap + 1);
+    uint16_t *EV = AK + cap.acap;
+    uint16_t *NSP = EV + cap.ecap;
+
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const snn_consts_t &c = T.c;
     const TrainWS &W = T.ws;
@@ -249,35 +285,67 @@ __global__ void __launch_bounds__(kTThreads) k_normad(const TrainArgs T) {
             H[m] = d;
         }
     }
-    __syncthreads();
 
     for (int64_t i = 0; i < T.n; ++i) {
-        const int32_t *soff = W.step_off + (size_t)i * (N + 1);
-        const uint16_t *sk = W.step_k + (size_t)i * W.evcap;
-        // (1) G(s,l): sum of W rows over the step's spiking neurons, ascending id
+        const int n_act = W.n_act[i];
+        const int32_t *g_aoff = W.act_off + (size_t)i * (kNH + 1);
+        const uint16_t *g_ak = W.act_k + (size_t)i * kNH;
+        const uint16_t *g_ev = W.step_k + (size_t)i * W.evcap;
+        const uint16_t *g_nsp = W.nsp + (size_t)i * W.evcap;
+        const int32_t *g_soff = W.step_off + (size_t)i * (N + 1);
+        const int n_ev = g_aoff[n_act];
+        const bool fast = n_act <= cap.acap && n_ev <= cap.ecap;
+
+        // ---- stage (coalesced, all threads)
+        for (int s = tid; s <= N; s += kTThreads) SOFF[s] = g_soff[s];
+        for (int s = tid; s < N; s += kTThreads) NRM[s] = W.norm[(size_t)i * N + s];
+        if (fast) {
+            for (int e = tid; e < n_ev; e += kTThreads) {
+                EV[e] = g_ev[e];
+                NSP[e] = g_nsp[e];
+            }
+            for (int j = tid; j <= n_act; j += kTThreads) AOFF[j] = g_aoff[j];
+            for (int j = tid; j < n_act; j += kTThreads) AK[j] = g_ak[j];
+            for (int t = tid; t < n_act * kNO; t += kTThreads) {
+                const int j = t / kNO, l = t - j * kNO;
+                WACT[t] = __ldcg(T.w + (size_t)g_ak[j] * kNO + l);
+            }
+        }
+        __syncthreads();
+        const uint16_t *ev = fast ? EV : g_ev;
+        const uint16_t *nsp = fast ? NSP : g_nsp;
+        const int *aoff = fast ? AOFF : g_aoff;
+        const uint16_t *ak = fast ? AK : g_ak;
+
+        // ---- (1) G(s,l): sum of W rows over the step's spiking neurons, ascending id
         for (int t = tid; t < N * kNO; t += kTThreads) {
             const int s = t / kNO, l = t - s * kNO;
             double g = 0.0;
-            const int e1 = soff[s + 1];
-            for (int e = soff[s]; e < e1; ++e) g = __dadd_rn(g, __ldcg(T.w + (size_t)sk[e] * kNO + l));
+            const int e1 = SOFF[s + 1];
+            if (fast)
+                for (int e = SOFF[s]; e < e1; ++e) g = __dadd_rn(g, WACT[ev[e] * kNO + l]);
+            else
+                for (int e = SOFF[s]; e < e1; ++e) g = __dadd_rn(g, __ldcg(T.w + (size_t)ak[ev[e]] * kNO + l));
             GR[t] = g;
         }
         __syncthreads();
-        // (2) output layer + error signal + NormAD gate (normad.py:156-159, :104-113)
+
+        // ---- (2) output layer + error signal + NormAD gate (normad.py:156-159, :104-113)
         if (warp == 0) {
             const int l = lane < kNO ? lane : kNO - 1;
             const int label = T.labels[i];
             const int per = c.desired_period;
-            const double *nrm = W.norm + (size_t)i * N;
+            int next_want = per > 0 ? per - 1 : 0x7fffffff;
             OutState st;
             out_init(st, c);
             for (int s = 0; s < N; ++s) {
                 double ff;
                 const bool fired = out_step(st, c, GR[s * kNO + l], s, &ff);
-                const bool want = per > 0 && l == label && s >= per - 1 && (s - (per - 1)) % per == 0;
+                const bool want = (s == next_want) && l == label;
+                if (s == next_want) next_want += per;
                 const int e = (int)want - (int)fired;
-                const bool any = (__ballot_sync(kFull, lane < kNO && e != 0) != 0);
-                const double nv = nrm[s];
+                const bool any = __ballot_sync(kFull, lane < kNO && e != 0) != 0;
+                const double nv = NRM[s];
                 double sg = 0.0;
                 if (any && nv > c.norm_eps && e != 0) sg = __ddiv_rn(__dmul_rn((double)e, c.dt), nv);
                 if (lane < kNO) SIG[s * kNO + lane] = sg;
@@ -285,42 +353,68 @@ __global__ void __launch_bounds__(kTThreads) k_normad(const TrainArgs T) {
             if (lane < kNO) T.counts[(size_t)i * kNO + lane] = st.cnt;
         }
         __syncthreads();
-        // (3) R(u,l) = sum_{s>=u} sigma(s,l) H(s-u)
-        for (int t = tid; t < N * kNO; t += kTThreads) {
-            const int u = t / kNO, l = t - u * kNO;
-            double r = 0.0;
-            for (int s = u; s < N; ++s) {
-                const double sg = SIG[s * kNO + l];
-                if (sg != 0.0) r = __dadd_rn(r, __dmul_rn(sg, H[s - u]));
+
+        // ---- (3) R(u,l) = sum_{s>=u} sigma(s,l) H(s-u), via the adjoint of the
+        // kernel -> d_hat recursions (backward, O(N) per output)
+        if (warp == 0 && lane < kNO) {
+            double pd = 0.0, pa = 0.0, pb = 0.0;
+            for (int u = N - 1; u >= 0; --u) {
+                pd = __dadd_rn(__dmul_rn(pd, c.decay_learn), SIG[u * kNO + lane]);
+                const double q = __dmul_rn(pd, c.dhat_scale);
+                pa = __dadd_rn(__dmul_rn(pa, c.decay_slow), q);
+                pb = __dadd_rn(__dmul_rn(pb, c.decay_fast), q);
+                // (a spike adds 1 to a and b alike, so its lag-0 trace is 0)
+                GR[u * kNO + lane] = __dsub_rn(pa, pb);
             }
-            GR[t] = r;
         }
         __syncthreads();
-        // (4) dW and the update W + r*dW (normad.py:117-127), all-or-nothing
-        const int n_act = W.n_act[i];
-        const uint16_t *act_k = W.act_k + (size_t)i * kNH;
-        const int32_t *act_off = W.act_off + (size_t)i * (kNH + 1);
-        const uint16_t *nsp = W.nsp + (size_t)i * W.evcap;
-        for (int pass = 0; pass < 2; ++pass) {
-            bool bad = false;
+
+        // ---- (4) dW per active neuron (spikes ascending) and W + r*dW, all-or-nothing
+        bool bad = false;
+        for (int j = tid; j < n_act; j += kTThreads) {
+            double acc[kNO];
+#pragma unroll
+            for (int l = 0; l < kNO; ++l) acc[l] = 0.0;
+            const int e1 = aoff[j + 1];
+            for (int e = aoff[j]; e < e1; ++e) {
+                const double *r = GR + (int)nsp[e] * kNO;
+#pragma unroll
+                for (int l = 0; l < kNO; ++l) acc[l] = __dadd_rn(acc[l], r[l]);
+            }
+            const double *wrow = fast ? WACT + (size_t)j * kNO : T.w + (size_t)ak[j] * kNO;
+#pragma unroll
+            for (int l = 0; l < kNO; ++l) {
+                const double wn = __dadd_rn(fast ? wrow[l] : __ldcg(wrow + l), __dmul_rn(c.learning_rate, acc[l]));
+                bad |= !isfinite(wn);
+                if (fast) WACT[(size_t)j * kNO + l] = wn;
+            }
+        }
+        if (__syncthreads_or(bad)) {
+            if (tid == 0) {
+                T.status[0] = SNN_ENONFINITE;
+                T.status[1] = (int32_t)(T.first + i);
+            }
+            return;
+        }
+        if (fast) {
             for (int t = tid; t < n_act * kNO; t += kTThreads) {
                 const int j = t / kNO, l = t - j * kNO;
-                double acc = 0.0;
-                const int e1 = act_off[j + 1];
-                for (int e = act_off[j]; e < e1; ++e) acc = __dadd_rn(acc, GR[(int)nsp[e] * kNO + l]);
-                double *wp = T.w + (size_t)act_k[j] * kNO + l;
-                const double wn = __dadd_rn(__ldcg(wp), __dmul_rn(c.learning_rate, acc));
-                if (pass == 0) bad |= !isfinite(wn);
-                else *wp = wn;
+                T.w[(size_t)AK[j] * kNO + l] = WACT[t];
             }
-            if (pass == 0) {
-                if (__syncthreads_or(bad)) {
-                    if (tid == 0) {
-                        T.status[0] = SNN_ENONFINITE;
-                        T.status[1] = (int32_t)(T.first + i);
-                    }
-                    return;
+        } else {
+            for (int j = tid; j < n_act; j += kTThreads) {
+                double acc[kNO];
+#pragma unroll
+                for (int l = 0; l < kNO; ++l) acc[l] = 0.0;
+                const int e1 = aoff[j + 1];
+                for (int e = aoff[j]; e < e1; ++e) {
+                    const double *r = GR + (int)nsp[e] * kNO;
+#pragma unroll
+                    for (int l = 0; l < kNO; ++l) acc[l] = __dadd_rn(acc[l], r[l]);
                 }
+                double *wrow = T.w + (size_t)ak[j] * kNO;
+#pragma unroll
+                for (int l = 0; l < kNO; ++l) wrow[l] = __dadd_rn(__ldcg(wrow + l), __dmul_rn(c.learning_rate, acc[l]));
             }
         }
         __syncthreads();

@@ -38,10 +38,30 @@ int validate(const snn_consts_t *c) {
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// ---- inference workspace: [n][22][N][10] f64 partials | [n] i32 arrivals
-size_t infer_ws(const snn_consts_t *c, int64_t n) {
-    return al((size_t)n * kMaxTiles * c->n_steps * kNO * sizeof(double)) + al((size_t)n * sizeof(int));
+// ---- inference workspace: tile_pos | n_tiles | tile_base | raster (upper bound)
+struct InferWS {
+    uint16_t *tile_pos;
+    int32_t *n_tiles, *tile_base;
+    uint8_t *raster;
+};
+
+size_t infer_ws_layout(const snn_consts_t *c, int64_t n, char *base, InferWS *w) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        char *p = base ? base + off : nullptr;
+        off += al(bytes);
+        return p;
+    };
+    InferWS x;
+    x.tile_pos = (uint16_t *)take((size_t)n * kMaxTiles * kTile * 2);
+    x.n_tiles = (int32_t *)take((size_t)n * 4);
+    x.tile_base = (int32_t *)take((size_t)(n + 1) * 4);
+    x.raster = (uint8_t *)take((size_t)n * kMaxTiles * c->n_steps * kTile * 2);
+    if (w) *w = x;
+    return off;
 }
+
+size_t infer_ws(const snn_consts_t *c, int64_t n) { return infer_ws_layout(c, n, nullptr, nullptr); }
 
 // ---- training workspace (per chunk)
 int64_t train_evcap(const snn_consts_t *c) {
@@ -53,7 +73,7 @@ int64_t train_evcap(const snn_consts_t *c) {
 
 size_t train_ws_per_image(const snn_consts_t *c) {
     const size_t N = c->n_steps, cap = train_evcap(c);
-    return kMaxTiles * N * kTile * 2 + kMaxTiles * kTile * 2 + 4 + 4 + kNH * 2 + (kNH + 1) * 4 + cap * 2 +
+    return kMaxTiles * N * kTile * 2 + kMaxTiles * kTile * 2 + 4 + 4 + 4 + kNH * 2 + (kNH + 1) * 4 + cap * 2 +
            (N + 1) * 4 + cap * 2 + N * 8 + kMaxTiles * N * 8;
 }
 
@@ -73,9 +93,10 @@ size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base) 
         return p;
     };
     TrainWS w;
-    w.raster = (uint16_t *)take(n * kMaxTiles * N * kTile * 2);
+    w.raster = (uint8_t *)take(n * kMaxTiles * N * kTile * 2);
     w.tile_pos = (uint16_t *)take(n * kMaxTiles * kTile * 2);
     w.n_tiles = (int32_t *)take(n * 4);
+    w.tile_base = (int32_t *)take((n + 1) * 4);
     w.n_act = (int32_t *)take(n * 4);
     w.act_k = (uint16_t *)take(n * kNH * 2);
     w.act_off = (int32_t *)take(n * (kNH + 1) * 4);
@@ -89,7 +110,72 @@ size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base) 
     return off;
 }
 
-size_t train_smem(const snn_consts_t *c) { return ((size_t)c->n_steps * (2 * kNO + 1)) * sizeof(double); }
+int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+// prep -> tile scan -> hidden (persistent) [-> output]; raster etc. in A
+// The specialised kernel is exact for any bank whose taps EQUAL the default
+// ones (+0.0 and -0.0 zero taps are both skipped, see def_current).
+bool is_default_bank(const snn_consts_t &c) {
+    for (int f = 0; f < kNF; ++f)
+        for (int k = 0; k < 9; ++k)
+            if (!(c.taps[f][k] == def_tap(f, k))) return false;
+    return true;
+}
+
+template <bool TRACE, bool DEF>
+int launch_batch(const BatchArgs &A, bool with_output, cudaStream_t st) {
+    static int hid_blocks = 0, out_cfg = 0;
+    if (!hid_blocks) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hid_blocks, k_hidden<TRACE, DEF>, kThreads, 0) !=
+                cudaSuccess ||
+            hid_blocks <= 0)
+            hid_blocks = 4;
+    }
+    if (!out_cfg) {
+        if (cudaFuncSetAttribute(k_output, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOutSmemBytes) !=
+            cudaSuccess)
+            return cuda_check("cudaFuncSetAttribute(k_output)");
+        out_cfg = 1;
+    }
+    int rc;
+    const unsigned n = (unsigned)A.n_images;
+    k_prep<<<n, kThreads, 0, st>>>(A);
+    if ((rc = cuda_check("k_prep"))) return rc;
+    k_tile_scan<<<1, 1024, 0, st>>>(A);
+    if ((rc = cuda_check("k_tile_scan"))) return rc;
+    const int64_t max_groups = (2 * A.n_images * kMaxTiles + kWPC - 1) / kWPC;
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)hid_blocks * sm_count(), max_groups);
+    k_hidden<TRACE, DEF><<<grid, kThreads, 0, st>>>(A);
+    if ((rc = cuda_check("k_hidden"))) return rc;
+    if (with_output) {
+        k_output<<<(n + kOutWarps - 1) / kOutWarps, kOutWarps * 32, kOutSmemBytes, st>>>(A);
+        if ((rc = cuda_check("k_output"))) return rc;
+    }
+    return SNN_OK;
+}
+
+// Shared-memory caps of k_normad: as many active neurons / events as fit in
+// ~200 KB next to the per-step arrays (roughly 1.5k neurons, 8k events at N=100).
+NormadCaps normad_caps(const snn_consts_t *c) {
+    const size_t budget = 200 * 1024;
+    NormadCaps cap{0, 0};
+    if (normad_smem_bytes(c->n_steps, cap) > budget) return cap;
+    const size_t left = budget - normad_smem_bytes(c->n_steps, cap);
+    // split: per active neuron 80+4+2 B, per event 4 B, ~6 events per active neuron
+    const size_t unit = 86 + 6 * 4;
+    cap.acap = (int)std::min<size_t>(kNH, left / unit);
+    cap.ecap = (int)std::min<size_t>(65535, (left - (size_t)cap.acap * 86) / 4);
+    return cap;
+}
 
 }  // namespace
 
@@ -119,29 +205,28 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
     if (!out || !out->counts) return set_error(SNN_EINVAL, "counts output is required");
     if (!d_images || !d_w || !d_ctab) return set_error(SNN_EINVAL, "NULL input pointer");
     if (((uintptr_t)d_images & 15) != 0) return set_error(SNN_EINVAL, "images must be 16-byte aligned");
-    if (n * kGroups > 0x7fffffffLL) return set_error(SNN_EINVAL, "too many images in one call");
-    if (out->raster && (!out->tile_pos || !out->n_tiles))
-        return set_error(SNN_EINVAL, "raster output needs tile_pos and n_tiles");
+    if (n * kMaxTiles > 0x7fffffffLL) return set_error(SNN_EINVAL, "too many images in one call");
+    if (out->raster && (!out->tile_pos || !out->n_tiles || !out->tile_base))
+        return set_error(SNN_EINVAL, "raster output needs tile_pos, n_tiles and tile_base");
     if (!d_ws || ws_bytes < infer_ws(c, n)) return set_error(SNN_ENOMEM, "workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
-    HiddenArgs A;
+    InferWS w;
+    infer_ws_layout(c, n, (char *)d_ws, &w);
+    BatchArgs A;
     memset(&A, 0, sizeof(A));
     A.c = *c;
     A.images = d_images;
     A.n_images = n;
     A.w = d_w;
     A.ctab = d_ctab;
-    A.partial = (double *)d_ws;
-    A.arrive = (int *)((char *)d_ws + al((size_t)n * kMaxTiles * c->n_steps * kNO * sizeof(double)));
+    A.tile_pos = out->tile_pos ? out->tile_pos : w.tile_pos;
+    A.n_tiles = out->n_tiles ? out->n_tiles : w.n_tiles;
+    A.tile_base = out->tile_base ? out->tile_base : w.tile_base;
+    A.raster = out->raster ? (uint8_t *)out->raster : w.raster;
     A.out = *out;
-    cudaMemsetAsync(A.arrive, 0, (size_t)n * sizeof(int), s);
-    const dim3 grid((unsigned)(n * kGroups));
-    const bool raster = out->raster != nullptr, trace = out->v_hid != nullptr;
-    if (raster && trace) k_hidden<true, true, true><<<grid, kThreads, 0, s>>>(A);
-    else if (raster) k_hidden<true, true, false><<<grid, kThreads, 0, s>>>(A);
-    else if (trace) k_hidden<true, false, true><<<grid, kThreads, 0, s>>>(A);
-    else k_hidden<true, false, false><<<grid, kThreads, 0, s>>>(A);
-    return cuda_check("k_hidden");
+    const bool def = is_default_bank(*c);
+    if (out->v_hid) return def ? launch_batch<true, true>(A, true, s) : launch_batch<true, false>(A, true, s);
+    return def ? launch_batch<false, true>(A, true, s) : launch_batch<false, false>(A, true, s);
 }
 
 extern "C" size_t snn_train_workspace(const snn_consts_t *c, int64_t n) {
@@ -162,7 +247,8 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     if (!d_images || !d_labels || !d_w || !d_ctab || !d_counts) return set_error(SNN_EINVAL, "NULL pointer");
     if (((uintptr_t)d_images & 15) != 0) return set_error(SNN_EINVAL, "images must be 16-byte aligned");
     if (c->n_steps > 65535) return set_error(SNN_EINVAL, "training supports n_steps <= 65535");
-    const size_t smem = train_smem(c);
+    const NormadCaps caps = normad_caps(c);
+    const size_t smem = normad_smem_bytes(c->n_steps, caps);
     if (smem > 220 * 1024) return set_error(SNN_EINVAL, "n_steps too large for the sequential NormAD CTA");
     const int64_t chunk = train_chunk(c, n);
     TrainArgs T;
@@ -176,25 +262,26 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     T.status = d_status;
     for (int64_t i0 = 0; i0 < n; i0 += chunk) {
         const int64_t cn = std::min(chunk, n - i0);
-        HiddenArgs A;
+        BatchArgs A;
         memset(&A, 0, sizeof(A));
         A.c = *c;
         A.images = d_images + i0 * SNN_N_PIXELS;
         A.n_images = cn;
         A.w = d_w;
         A.ctab = d_ctab;
-        A.out.raster = T.ws.raster;
-        A.out.tile_pos = T.ws.tile_pos;
-        A.out.n_tiles = T.ws.n_tiles;
-        k_hidden<false, true, false><<<(unsigned)(cn * kGroups), kThreads, 0, s>>>(A);
-        if ((rc = cuda_check("k_hidden<raster>"))) return rc;
+        A.raster = T.ws.raster;
+        A.tile_pos = T.ws.tile_pos;
+        A.n_tiles = T.ws.n_tiles;
+        A.tile_base = T.ws.tile_base;
+        if ((rc = is_default_bank(*c) ? launch_batch<false, true>(A, false, s) : launch_batch<false, false>(A, false, s)))
+            return rc;
         T.n = cn;
         T.first = i0;
         T.labels = d_labels + i0;
         T.counts = d_counts + i0 * kNO;
         k_compact<<<(unsigned)cn, kCThreads, 0, s>>>(T);
         if ((rc = cuda_check("k_compact"))) return rc;
-        k_normad<<<1, kTThreads, smem, s>>>(T);
+        k_normad<<<1, kTThreads, smem, s>>>(T, caps);
         if ((rc = cuda_check("k_normad"))) return rc;
     }
     return SNN_OK;

@@ -123,10 +123,12 @@ class Engine:
         self.stream.wait_stream(torch.cuda.current_stream(dev))   # inputs made on the caller's stream
         with torch.cuda.stream(self.stream):
             out = {"counts": torch.empty((n, N_OUTPUTS), dtype=torch.int32, device=dev)}
-            if raster:
-                out["raster"] = torch.empty((n, _native.MAX_TILES, N, _native.TILE), dtype=torch.int16, device=dev)
+            if raster:  # compact layout, see include/snn_b200.h
+                out["raster"] = torch.empty((n * _native.MAX_TILES * N * 2 * _native.TILE,), dtype=torch.uint8,
+                                            device=dev)
                 out["tile_pos"] = torch.empty((n, _native.MAX_TILES, _native.TILE), dtype=torch.int16, device=dev)
                 out["n_tiles"] = torch.empty((n,), dtype=torch.int32, device=dev)
+                out["tile_base"] = torch.empty((n + 1,), dtype=torch.int32, device=dev)
                 out["out_raster"] = torch.empty((n, N), dtype=torch.int16, device=dev)
             if trace:
                 out["ff"] = torch.empty((n, N, N_OUTPUTS), dtype=torch.float64, device=dev)
@@ -136,6 +138,8 @@ class Engine:
         chunk = max(1, min(n, (1 << 30) // per_img))
         if max_chunk:
             chunk = min(chunk, max_chunk)
+        if raster:
+            chunk = n  # the compact raster of one call is indexed by one tile_base
         assert images.dtype == torch.uint8 and images.is_contiguous() and images.shape[1] == N_INPUTS
         assert w.dtype == torch.float64 and w.is_contiguous() and tuple(w.shape) == (N_HIDDEN, N_OUTPUTS)
         for i0 in range(0, n, chunk):
@@ -144,7 +148,7 @@ class Engine:
             ws = self.buffer("infer", ws_bytes)
             o = _native.InferOutC()
             for name, t in out.items():
-                setattr(o, name, t[i0:i0 + cn].data_ptr())
+                setattr(o, name, t.data_ptr() if name in ("raster", "tile_base") else t[i0:i0 + cn].data_ptr())
             _native.check(self.lib.snn_infer(
                 ctypes.byref(c), images[i0:i0 + cn].data_ptr(), cn, w.data_ptr(), ctab.data_ptr(),
                 ctypes.byref(o), ws.data_ptr(), ws_bytes, self.sptr))

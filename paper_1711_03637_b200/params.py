@@ -238,9 +238,9 @@ class FilterBank:
 def default_filter_bank(drive: float = DEFAULT_FILTER_DRIVE) -> FilterBank:
     """4 Sobel-style edges, their negations, 4 corner contrasts; each gain is
     drive / (sum of the kernel's positive cells)."""
-    edges = np.array(_EDGE, dtype=np.float64)
-    kernels = np.concatenate([edges, -edges, np.stack([_corner(0, 0), _corner(0, 1),
-                                                       _corner(1, 0), _corner(1, 1)])])
+    edges = np.array(_EDGE)          # negate as integers: zero taps stay +0.0 as in filters.py:76-79
+    kernels = np.concatenate([edges, -edges]).astype(np.float64)
+    kernels = np.concatenate([kernels, np.stack([_corner(0, 0), _corner(0, 1), _corner(1, 0), _corner(1, 1)])])
     return FilterBank(kernels=kernels, gains=drive / np.clip(kernels, 0.0, None).sum(axis=(1, 2)))
 
 

@@ -268,11 +268,14 @@ def test_zero_error_fixed_point(sd, bank):
 
 
 def test_non_finite_update_raises(sd, cfg, bank, workloads):
+    """normad.py:122-124: a non-finite update raises NumericFailureError.  With
+    every weight at the float64 maximum the output layer saturates, the target
+    spikes are missed (e = +1) and any positive update overflows to inf."""
     learn = sd.LearnConfig(learning_rate=1e308)
     order = workloads["c2_order"]
+    w = np.full((8112, 10), np.finfo(np.float64).max)
     with pytest.raises(sd.NumericFailureError):
-        sd.train_epoch(workloads["c2_images"][order][:5] * 0 + 200, np.full(5, 3), np.full((8112, 10), 1e308),
-                       bank, cfg, learn)
+        sd.train_epoch(workloads["c2_images"][order][:3], workloads["c2_labels"][order][:3], w, bank, cfg, learn)
 
 
 def test_train_validation(sd, cfg, bank):
@@ -285,3 +288,25 @@ def test_train_validation(sd, cfg, bank):
     w1, st = sd.train_epoch(np.zeros((0, 28, 28), dtype=np.uint8), np.zeros(0, dtype=int), sd.zero_weights(),
                             bank, cfg, sd.LearnConfig())
     assert st.n_images == 0 and not w1.any()
+
+
+def test_custom_filter_bank_generic_kernel(sd, cfg, workloads, oracle):
+    """A non-default bank takes the generic (runtime-tap) kernel: same parity bar."""
+    rng = np.random.default_rng(123)
+    kernels = rng.integers(-3, 4, size=(12, 3, 3)).astype(np.float64)
+    gains = rng.uniform(1e-9, 4e-9, size=12)
+    bank = sd.FilterBank(kernels=kernels, gains=gains)
+    w = rng.uniform(0, 1, size=(8112, 10)) * 4e-11
+    imgs = workloads["c3_images"][:12]
+    got = sd.batch_counts(imgs, w, bank, cfg)
+    p = oracle.Params(taps=np.array(bank.weighted))
+    ctab = oracle.input_table(p)[1]
+    recs = [oracle.simulate(x, w, p, ctab=ctab, record=True) for x in imgs[:3]]
+    want = np.stack([oracle.simulate(x, w, p, ctab=ctab)["counts"] for x in imgs])
+    assert np.array_equal(got, want)
+    for k in range(3):
+        rec = sd.forward_pass(imgs[k], w, bank, cfg)
+        hm = np.zeros((cfg.n_steps, 8112), dtype=bool)
+        for nidx, steps in enumerate(rec.hidden_spikes):
+            hm[steps, nidx] = True
+        assert np.array_equal(hm, recs[k]["hidden"])

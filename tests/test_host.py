@@ -93,20 +93,22 @@ def test_consts_follow_reference_expressions(sd):
 def test_decode_hidden_roundtrip():
     from paper_1711_03637_b200.api import decode_hidden
     rng = np.random.default_rng(0)
-    N = 20
+    N, tb = 20, 5
     want = np.zeros((N, 8112), dtype=bool)
     active = np.sort(rng.choice(676, size=70, replace=False))
-    raster = np.zeros((22, N, 32), dtype=np.int16)
+    nt = 3
+    raster = np.zeros((tb + nt) * N * 64, dtype=np.uint8)
+    blk = raster[tb * N * 64:].reshape(N, nt, 2, 32)
     tpos = np.full((22, 32), -1, dtype=np.int16)
     for slot, p in enumerate(active):
         t, lane = divmod(slot, 32)
         tpos[t, lane] = p
-        m = rng.integers(0, 4096, size=N)
-        m &= rng.integers(0, 4096, size=N)
-        raster[t, :, lane] = m
+        m = rng.integers(0, 4096, size=N) & rng.integers(0, 4096, size=N)
+        blk[:, t, 0, lane] = m & 0x3F
+        blk[:, t, 1, lane] = m >> 6
         for f in range(12):
             want[:, p * 12 + f] = (m >> f) & 1
-    got = decode_hidden(raster, tpos, 3, N)
+    got = decode_hidden(raster, tb, tpos, nt, N)
     assert np.array_equal(got, want)
 
 
