@@ -249,6 +249,7 @@ __host__ __device__ inline size_t normad_smem_bytes(int N, NormadCaps cap) {
     b += (size_t)N * 8 * 2;                  // H, NRM
     b += (size_t)cap.acap * kNO * 8;         // WACT
     b += ((size_t)N + 1) * 4;                // SOFF
+    b += (size_t)N * 2;                      // OMASK
     b += ((size_t)cap.acap + 1) * 4;         // AOFF
     b += (size_t)cap.acap * 2;               // AK
     b += (size_t)cap.ecap * 2 * 2;           // EV, NSP
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(kTThreads) k_normad(const TrainArgs T, const N
     uint16_t *AK = reinterpret_cast<uint16_t *>(AOFF + cap.acap + 1);
     uint16_t *EV = AK + cap.acap;
     uint16_t *NSP = EV + cap.ecap;
+    uint16_t *OMASK = NSP + cap.ecap;              // output spikes of each step (10-bit)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const snn_consts_t &c = T.c;
@@ -330,27 +332,38 @@ __global__ void __launch_bounds__(kTThreads) k_normad(const TrainArgs T, const N
         }
         __syncthreads();
 
-        // ---- (2) output layer + error signal + NormAD gate (normad.py:156-159, :104-113)
+        // ---- (2) output layer (network.py:308-314): the only serial chain.  The
+        // error signal and gate are evaluated afterwards in parallel.
         if (warp == 0) {
             const int l = lane < kNO ? lane : kNO - 1;
-            const int label = T.labels[i];
-            const int per = c.desired_period;
-            int next_want = per > 0 ? per - 1 : 0x7fffffff;
             OutState st;
             out_init(st, c);
             for (int s = 0; s < N; ++s) {
                 double ff;
                 const bool fired = out_step(st, c, GR[s * kNO + l], s, &ff);
-                const bool want = (s == next_want) && l == label;
-                if (s == next_want) next_want += per;
-                const int e = (int)want - (int)fired;
-                const bool any = __ballot_sync(kFull, lane < kNO && e != 0) != 0;
-                const double nv = NRM[s];
-                double sg = 0.0;
-                if (any && nv > c.norm_eps && e != 0) sg = __ddiv_rn(__dmul_rn((double)e, c.dt), nv);
-                if (lane < kNO) SIG[s * kNO + lane] = sg;
+                const unsigned om = __ballot_sync(kFull, fired) & 0x3FFu;
+                if (lane == 0) OMASK[s] = (uint16_t)om;
             }
             if (lane < kNO) T.counts[(size_t)i * kNO + lane] = st.cnt;
+        }
+        __syncthreads();
+        // error signal, gate and normalised step (normad.py:156-159, :87-91, :104-113):
+        // e = desired - observed; a step counts if any e != 0 and |d_hat| > eps;
+        // sigma(s,l) = (e_l * dt) / |d_hat(s)|
+        {
+            const int label = T.labels[i];
+            const int per = c.desired_period;
+            for (int t = tid; t < N * kNO; t += kTThreads) {
+                const int s = t / kNO, l = t - s * kNO;
+                const bool want_step = per > 0 && s >= per - 1 && (s - (per - 1)) % per == 0;
+                const unsigned wmask = want_step ? (1u << label) : 0u;
+                const unsigned om = OMASK[s];
+                const int e = (int)((wmask >> l) & 1u) - (int)((om >> l) & 1u);
+                const double nv = NRM[s];
+                double sg = 0.0;
+                if (om != wmask && nv > c.norm_eps && e != 0) sg = __ddiv_rn(__dmul_rn((double)e, c.dt), nv);
+                SIG[t] = sg;
+            }
         }
         __syncthreads();
 

@@ -50,3 +50,33 @@ extern "C" int snn_measure_fma_peaks(double *tflops_fp64, double *tflops_fp32) {
     *tflops_fp32 = run<float>(1 << 15);
     return cudaGetLastError() == cudaSuccess ? 0 : 1002;
 }
+
+// Dependent-chain latency of one FP64 add/mul (cycles), single thread.
+__global__ void k_dp_latency(double *out, long long *cycles, int iters, double a, double b) {
+    double x = out[0];
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+        x = __dadd_rn(x, a);
+        x = __dmul_rn(x, b);
+    }
+    const long long t1 = clock64();
+    out[1] = x;
+    cycles[0] = t1 - t0;
+}
+
+extern "C" int snn_measure_dp_latency(double *cycles_per_op) {
+    double *out;
+    long long *cyc;
+    cudaMalloc(&out, 2 * sizeof(double));
+    cudaMalloc(&cyc, sizeof(long long));
+    cudaMemset(out, 0, 2 * sizeof(double));
+    const int iters = 4096;
+    k_dp_latency<<<1, 1>>>(out, cyc, iters, 1e-3, 0.999);
+    k_dp_latency<<<1, 1>>>(out, cyc, iters, 1e-3, 0.999);
+    long long c = 0;
+    cudaMemcpy(&c, cyc, sizeof(c), cudaMemcpyDeviceToHost);
+    cudaFree(out);
+    cudaFree(cyc);
+    *cycles_per_op = (double)c / (2.0 * iters);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1002;
+}

@@ -222,7 +222,7 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
     A.tile_pos = out->tile_pos ? out->tile_pos : w.tile_pos;
     A.n_tiles = out->n_tiles ? out->n_tiles : w.n_tiles;
     A.tile_base = out->tile_base ? out->tile_base : w.tile_base;
-    A.raster = out->raster ? (uint8_t *)out->raster : w.raster;
+    A.raster = out->raster ? out->raster : w.raster;
     A.out = *out;
     const bool def = is_default_bank(*c);
     if (out->v_hid) return def ? launch_batch<true, true>(A, true, s) : launch_batch<true, false>(A, true, s);

@@ -114,7 +114,8 @@ class Engine:
     def infer(self, c, images, w, *, raster=False, trace=False, max_chunk=None):
         """Run n presentations.  images: uint8 [n,784] device tensor; w: f64
         [8112,10] device tensor.  Returns dict of device tensors (counts int32
-        [n,10]; optionally raster/tile_pos/n_tiles/out_raster, ff/v_out/v_hid)."""
+        [n,10]; optionally raster/tile_pos/n_tiles/tile_base/out_raster,
+        ff/v_out/v_hid)."""
         torch = _torch()
         n = int(images.shape[0])
         N = c.n_steps
@@ -148,7 +149,8 @@ class Engine:
             ws = self.buffer("infer", ws_bytes)
             o = _native.InferOutC()
             for name, t in out.items():
-                setattr(o, name, t.data_ptr() if name in ("raster", "tile_base") else t[i0:i0 + cn].data_ptr())
+                whole = name in ("raster", "tile_base")
+                setattr(o, name, t.data_ptr() if whole else t[i0:i0 + cn].data_ptr())
             _native.check(self.lib.snn_infer(
                 ctypes.byref(c), images[i0:i0 + cn].data_ptr(), cn, w.data_ptr(), ctab.data_ptr(),
                 ctypes.byref(o), ws.data_ptr(), ws_bytes, self.sptr))
