@@ -112,6 +112,12 @@ int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t n_images,
               const double *d_weights, const double *d_ctab, const snn_infer_out_t *out,
               void *d_workspace, size_t workspace_bytes, void *stream);
 
+/* Profiling hook: when set, every following snn_infer / snn_train call records
+ * `before` (a cudaEvent_t) on its stream just before the fused hidden-layer
+ * kernel (k_hidden) and `after` just after it, so a caller can time that
+ * kernel alone with cudaEventElapsedTime.  Pass NULLs to disable. */
+void snn_profile_events(void *before, void *after);
+
 /* Bytes of device workspace snn_train needs for n images. */
 size_t snn_train_workspace(const snn_consts_t *c, int64_t n_images);
 

@@ -62,6 +62,7 @@ SIGNATURES = [
     ("snn_infer_workspace", ctypes.c_size_t, [ctypes.POINTER(ConstsC), ctypes.c_int64]),
     ("snn_infer", ctypes.c_int, [ctypes.POINTER(ConstsC), _vp, ctypes.c_int64, _vp, _vp,
                                  ctypes.POINTER(InferOutC), _vp, ctypes.c_size_t, _vp]),
+    ("snn_profile_events", None, [_vp, _vp]),
     ("snn_train_workspace", ctypes.c_size_t, [ctypes.POINTER(ConstsC), ctypes.c_int64]),
     ("snn_train", ctypes.c_int, [ctypes.POINTER(ConstsC), _vp, _vp, ctypes.c_int64, _vp, _vp, _vp,
                                  _vp, _vp, ctypes.c_size_t, _vp]),

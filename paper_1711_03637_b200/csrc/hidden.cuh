@@ -60,6 +60,8 @@ struct BatchArgs {
     int32_t *n_tiles;        // [n]
     int32_t *tile_base;      // [n+1] exclusive prefix of n_tiles
     uint8_t *raster;         // sum(n_tiles) * N * 64 spike-mask bytes (see raster_at)
+    double *partial;         // [items][N][10] per-item G partials (inference)
+    int32_t items_per_tile;  // 1 (default bank) or 2 (generic bank)
     snn_infer_out_t out;     // counts / out_raster / ff / v_out / v_hid
 };
 
@@ -268,10 +270,102 @@ __device__ __forceinline__ unsigned hidden_step(const BatchArgs &A, const double
 // features, which keeps the 54 runtime taps of a warp within the register
 // budget.  The table chunks form one continuous stream across groups, so the
 // TMA ring never drains between groups.
-template <bool TRACE, bool DEF>
+// Per-item partial of G for the steps of one chunk: G_item(s, l) = sum of
+// W[k, l] over the item's neurons k spiking at s, in (lane, feature) order.
+// One packed warp scan lists the ids of all 8 steps; then lane (j, q) sums
+// step j's rows for outputs q, q+4, q+8 sequentially in list order (fixed
+// order: deterministic).  Done at the chunk end so the W loads of 8 steps
+// overlap other warps' FP64 work; an item's ~46 spiking neurons keep their W
+// rows in L1.
+constexpr int kPIds = 256;  // ids per chunk staged in shared memory
+
+__device__ __forceinline__ void chunk_partials(const BatchArgs &A, uint16_t *ids, int item, int s0, int nrows,
+                                               uint64_t mlo, uint64_t mhi, int id0) {
+    const int lane = threadIdx.x & 31;
+    const int N = A.c.n_steps;
+    double *P = A.partial + (size_t)item * N * kNO;
+    uint64_t cA = 0, cB = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        cA |= (uint64_t)__popc((unsigned)(mlo >> (16 * q)) & 0xFFFFu) << (16 * q);
+        cB |= (uint64_t)__popc((unsigned)(mhi >> (16 * q)) & 0xFFFFu) << (16 * q);
+    }
+    uint64_t tA, tB;
+    const uint64_t eA = warp_excl_scan_u64(cA, &tA), eB = warp_excl_scan_u64(cB, &tB);
+    int base[kChunk + 1];
+    base[0] = 0;
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j)
+        base[j + 1] = base[j] + (int)(((j < 4 ? tA : tB) >> (16 * (j & 3))) & 0xFFFF);
+    const int total = base[kChunk];
+    const int jj = lane >> 2, q = lane & 3;  // lane -> (step jj, outputs q, q+4, q+8)
+    if (total <= kPIds) {
+        if (total) {
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j) {
+                unsigned mm = (unsigned)((j < 4 ? mlo : mhi) >> (16 * (j & 3))) & 0xFFFFu;
+                int k = base[j] + (int)(((j < 4 ? eA : eB) >> (16 * (j & 3))) & 0xFFFF);
+                while (mm) {
+                    const int f = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    ids[k++] = (uint16_t)(id0 + f);
+                }
+            }
+        }
+        __syncwarp();
+        if (jj < nrows) {
+            int lo = 0, hi = 0;
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j)
+                if (j == jj) {
+                    lo = base[j];
+                    hi = base[j + 1];
+                }
+            double g0 = 0.0, g1 = 0.0, g2 = 0.0;
+            for (int e = lo; e < hi; ++e) {
+                const double *row = A.w + (size_t)ids[e] * kNO;
+                g0 = __dadd_rn(g0, __ldg(row + q));
+                g1 = __dadd_rn(g1, __ldg(row + q + 4));
+                if (q < 2) g2 = __dadd_rn(g2, __ldg(row + q + 8));
+            }
+            double *dst = P + (size_t)(s0 + jj) * kNO;
+            dst[q] = g0;
+            dst[q + 4] = g1;
+            if (q < 2) dst[q + 8] = g2;
+        }
+        __syncwarp();
+        return;
+    }
+    // rare: more than kPIds spikes in one chunk of one item -- one step at a time, in windows
+    for (int j = 0; j < nrows; ++j) {
+        const unsigned m = (unsigned)((j < 4 ? mlo : mhi) >> (16 * (j & 3))) & 0xFFFFu;
+        int tot;
+        const int off = warp_excl_scan_int(__popc(m), &tot);
+        double g[3] = {0.0, 0.0, 0.0};
+        for (int w0 = 0; w0 < tot; w0 += kPIds) {
+            const int wn = min(kPIds, tot - w0);
+            int k = off - w0;
+            unsigned mm = m;
+            while (mm) {
+                const int f = __ffs(mm) - 1;
+                mm &= mm - 1;
+                if (k >= 0 && k < wn) ids[k] = (uint16_t)(id0 + f);
+                ++k;
+            }
+            __syncwarp();
+            if (lane < kNO)
+                for (int e = 0; e < wn; ++e) g[0] = __dadd_rn(g[0], __ldg(A.w + (size_t)ids[e] * kNO + lane));
+            __syncwarp();
+        }
+        if (lane < kNO) P[(size_t)(s0 + j) * kNO + lane] = g[0];
+    }
+}
+
+template <bool TRACE, bool DEF, bool RASTER, bool GSUM>
 __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
     __shared__ __align__(128) double s_tab[kStages][kChunk * 256];
     __shared__ uint64_t s_full[kStages];
+    __shared__ uint16_t s_ids[kWPC][kPIds];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = A.c.n_steps;
     const int nchunks = (N + kChunk - 1) / kChunk;
@@ -339,8 +433,10 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
             v[f] = el;
             live_from[f] = 0;
         }
-        uint8_t *rout = live ? A.raster + raster_at(A.tile_base[img], N, nt, 0, tile) + half * kTile + lane : nullptr;
+        uint8_t *rout = (RASTER && live) ? A.raster + raster_at(A.tile_base[img], N, nt, 0, tile) + half * kTile + lane
+                                         : nullptr;
         const size_t rstride = (size_t)nt * 2 * kTile;
+        const int id0 = pos * kNF + half * kHalf;
 
         for (int ch = 0; ch < nchunks; ++ch, ++q) {
             const int b = (int)(q % kStages);
@@ -348,6 +444,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
             const int nrows = min(kChunk, N - s0);
             if (live) {
                 mbar_wait(&s_full[b], (uint32_t)((q / kStages) & 1));
+                uint64_t mlo = 0, mhi = 0;  // the chunk's spike masks (16 bits per step)
 #pragma unroll 1
                 for (int j = 0; j < nrows; ++j) {
                     const int s = s0 + j;
@@ -365,9 +462,17 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
 #pragma unroll
                         for (int f = 0; f < (DEF ? kNF : kHalf); ++f) dst[f] = v[f];
                     }
-                    rout[(size_t)s * rstride] = (uint8_t)(m & 0x3Fu);
-                    if (DEF) rout[(size_t)s * rstride + kTile] = (uint8_t)(m >> kHalf);
+                    if (RASTER) {
+                        rout[(size_t)s * rstride] = (uint8_t)(m & 0x3Fu);
+                        if (DEF) rout[(size_t)s * rstride + kTile] = (uint8_t)(m >> kHalf);
+                    }
+                    if (GSUM) {
+                        const unsigned mo = on ? m : 0u;
+                        if (j < 4) mlo |= (uint64_t)mo << (16 * j);
+                        else mhi |= (uint64_t)mo << (16 * (j - 4));
+                    }
                 }
+                if (GSUM) chunk_partials(A, s_ids[warp], item, s0, nrows, mlo, mhi, id0);
             }
             __syncthreads();  // every warp is done with stage b
             if (tid == 0 && q + kStages < stream_len) issue(q + kStages);
@@ -378,36 +483,43 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
 // ---------------------------------------------------------------------------
 // Output layer state and one step of it (network.py:308-314), lanes 0..9 of
 // one warp = the 10 output neurons (lanes 10..31 shadow lane 9, harmlessly).
+// Every lane keeps all ten lateral-inhibition traces and advances them from
+// the previous step's spike ballot, so the inhibition sum needs no shuffles
+// on the serial path (same operations as the reference, so bit-identical).
 struct OutState {
-    double Af, Bf;   // event-driven feed-forward recursions (slow, fast)
-    double ao, bo;   // lateral-inhibition kernel of this output neuron
+    double Af, Bf;           // event-driven feed-forward recursions (slow, fast)
+    double ao[kNO], bo[kNO]; // lateral-inhibition kernels of all output neurons
     double v;
     int live_from, cnt;
-    bool prev;
+    unsigned prev;           // output spikes of the previous step (10-bit)
 };
 
 __device__ __forceinline__ void out_init(OutState &st, const snn_consts_t &c) {
-    st.Af = st.Bf = st.ao = st.bo = 0.0;
+    st.Af = st.Bf = 0.0;
+#pragma unroll
+    for (int k = 0; k < kNO; ++k) st.ao[k] = st.bo[k] = 0.0;
     st.v = c.lif_out.el;
     st.live_from = 0;
     st.cnt = 0;
-    st.prev = false;
+    st.prev = 0u;
 }
 
 // Advances one step given G (sum of W rows of hidden neurons spiking now).
-// Returns whether this lane's output neuron fired; *ff_out = c_hidden @ W.
-__device__ __forceinline__ bool out_step(OutState &st, const snn_consts_t &c, double G, int s,
+// Returns whether this lane's output neuron l fired; *ff_out = c_hidden @ W.
+__device__ __forceinline__ bool out_step(OutState &st, const snn_consts_t &c, double G, int s, int l,
                                          double *ff_out) {
     st.Af = __dadd_rn(__dmul_rn(st.Af, c.decay_slow), G);
     st.Bf = __dadd_rn(__dmul_rn(st.Bf, c.decay_fast), G);
     const double ff = __dsub_rn(st.Af, st.Bf);
-    const double bump = st.prev ? 1.0 : 0.0;  // inhibition sees last step's spikes
-    st.ao = __dadd_rn(__dmul_rn(st.ao, c.decay_slow), bump);
-    st.bo = __dadd_rn(__dmul_rn(st.bo, c.decay_fast), bump);
-    const double co = __dsub_rn(st.ao, st.bo);
-    double cc[kNO];
+    double cc[kNO], co = 0.0;
 #pragma unroll
-    for (int k = 0; k < kNO; ++k) cc[k] = __shfl_sync(kFull, co, k);
+    for (int k = 0; k < kNO; ++k) {  // inhibition sees last step's spikes
+        const double bump = ((st.prev >> k) & 1u) ? 1.0 : 0.0;
+        st.ao[k] = __dadd_rn(__dmul_rn(st.ao[k], c.decay_slow), bump);
+        st.bo[k] = __dadd_rn(__dmul_rn(st.bo[k], c.decay_fast), bump);
+        cc[k] = __dsub_rn(st.ao[k], st.bo[k]);
+        co = k == l ? cc[k] : co;
+    }
     const double S = pairwise10(cc);
     const double drive = __dadd_rn(ff, __dmul_rn(c.inhibition, __dsub_rn(S, co)));
     const double cand = lif_candidate(st.v, drive, c.lif_out);
@@ -415,26 +527,23 @@ __device__ __forceinline__ bool out_step(OutState &st, const snn_consts_t &c, do
     const bool fired = live && cand >= c.lif_out.vt;
     if (live) st.v = fired ? c.lif_out.el : cand;
     if (fired) st.live_from = next_live_step(s, c.lif_out.refr);
-    st.prev = fired;
+    st.prev = __ballot_sync(kFull, fired) & 0x3FFu;
     st.cnt += fired ? 1 : 0;
     *ff_out = ff;
     return fired;
 }
 
 // ---------------------------------------------------------------------------
-// k_output: one warp per image -- G from the raster and W, then the output
-// layer, one step at a time.  A step's raster segment is contiguous (nt x 64
-// bytes), so the warp loads it with 16-byte vector loads, lists the spiking
-// neurons in raster memory order (tile, half, lane, feature) with one popc +
-// one warp scan, and 30 lanes add their W rows: lane q*10+l sums a strided
-// third for output l, combined as (g0 + g1) + g2 -- a fixed order, so G is
-// deterministic.  W rows are plain L1-cached loads: an image's ~1,000
-// spiking neurons fire ~7 times each.  G(s) feeds the output layer directly.
-constexpr int kIdCap = 512;  // spike ids per round (a step has ~70 on MNIST-like input)
+// k_output: one warp per image -- G(s) = sum of the image's item partials in
+// item order, then the output layer.  For up to kOSteps steps at a time, lane
+// i computes G for steps i, i+32, ... (all 10 outputs, 80-byte partial rows
+// as double2 loads, all independent) into shared memory; then lanes 0..9 run
+// the sequential output layer from shared memory.
+constexpr int kOItems = 2 * kMaxTiles;
+constexpr int kOSteps = 96;
 
 struct OutSmem {
-    uint16_t pos[kMaxTiles * kTile];
-    uint16_t ids[kIdCap];
+    double2 G[kOSteps * 5];
 };
 
 __global__ void __launch_bounds__(kOutWarps * 32) k_output(const BatchArgs A) {
@@ -444,77 +553,43 @@ __global__ void __launch_bounds__(kOutWarps * 32) k_output(const BatchArgs A) {
     const int64_t img = (int64_t)blockIdx.x * kOutWarps + warp;
     if (img >= A.n_images) return;
     const int N = A.c.n_steps;
-    const int nt = A.n_tiles[img];
-    const int64_t tb = A.tile_base[img];
+    const int ni = A.n_tiles[img] * A.items_per_tile;
     const int l = lane < kNO ? lane : kNO - 1;
-    const int q3 = lane / kNO, lq = lane - q3 * kNO;
-    const double *W = A.w;
-    for (int k = lane; k < nt * kTile; k += 32) S.pos[k] = A.tile_pos[img * (kMaxTiles * kTile) + k];
-    __syncwarp();
-    const int nvec = nt * 4;  // uint4 per step segment (64 B per tile)
-    constexpr int kMaxVec = (kMaxTiles * 4 + 31) / 32;
-
+    const double2 *P = reinterpret_cast<const double2 *>(A.partial + (size_t)A.tile_base[img] * A.items_per_tile * N * kNO);
+    const size_t istride = (size_t)N * 5;  // double2 per item
+    const double *Gd = reinterpret_cast<const double *>(S.G);
     OutState st;
     out_init(st, A.c);
-    uint4 cur[kMaxVec], nxt[kMaxVec];
-    auto load_step = [&](int s, uint4 (&v)[kMaxVec]) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(A.raster + raster_at(tb, N, nt, s, 0));
+    for (int s0 = 0; s0 < N; s0 += kOSteps) {
+        const int ns = min(kOSteps, N - s0);
+        for (int j = lane; j < ns; j += 32) {
+            double2 g[5];
 #pragma unroll
-        for (int r = 0; r < kMaxVec; ++r) {
-            const int k = lane + 32 * r;
-            v[r] = k < nvec ? __ldcg(src + k) : make_uint4(0, 0, 0, 0);
-        }
-    };
-    if (N > 0) load_step(0, cur);
-    for (int s = 0; s < N; ++s) {
-        if (s + 1 < N) load_step(s + 1, nxt);
-        int c = 0;
+            for (int p = 0; p < 5; ++p) g[p] = make_double2(0.0, 0.0);
+            const double2 *src = P + (size_t)(s0 + j) * 5;
+            for (int i = 0; i < ni; ++i) {
 #pragma unroll
-        for (int r = 0; r < kMaxVec; ++r) c += __popc(cur[r].x) + __popc(cur[r].y) + __popc(cur[r].z) + __popc(cur[r].w);
-        int tot;
-        const int off = warp_excl_scan_int(c, &tot);
-        double G = 0.0;
-        for (int w0 = 0; w0 < tot; w0 += kIdCap) {  // rounds of kIdCap ids (one round in practice)
-            const int wn = min(kIdCap, tot - w0);
-            int k = off - w0;
-#pragma unroll
-            for (int r = 0; r < kMaxVec; ++r) {
-                const uint32_t wv[4] = {cur[r].x, cur[r].y, cur[r].z, cur[r].w};
-#pragma unroll
-                for (int wi = 0; wi < 4; ++wi) {
-                    uint32_t bits = wv[wi];
-                    while (bits) {
-                        const int b = __ffs(bits) - 1;
-                        bits &= bits - 1;
-                        if (k >= 0 && k < wn) {
-                            // byte index in the step segment -> (tile, half, lane), bit -> feature
-                            const int by = (lane + 32 * r) * 16 + wi * 4 + (b >> 3);
-                            const int t = by >> 6, half = (by >> 5) & 1, ln = by & 31;
-                            S.ids[k] = (uint16_t)(S.pos[t * kTile + ln] * kNF + half * kHalf + (b & 7));
-                        }
-                        ++k;
-                    }
+                for (int p = 0; p < 5; ++p) {
+                    const double2 a = __ldcg(src + i * istride + p);
+                    g[p].x = __dadd_rn(g[p].x, a.x);
+                    g[p].y = __dadd_rn(g[p].y, a.y);
                 }
             }
-            __syncwarp();
-            double g = 0.0;
-            if (q3 < 3)
-                for (int e = q3; e < wn; e += 3) g = __dadd_rn(g, __ldg(W + (size_t)S.ids[e] * kNO + lq));
-            const double g1 = __shfl_down_sync(kFull, g, kNO), g2 = __shfl_down_sync(kFull, g, 2 * kNO);
-            G = __dadd_rn(G, __dadd_rn(__dadd_rn(g, g1), g2));  // valid on lanes 0..9
-            __syncwarp();
-        }
-        G = __shfl_sync(kFull, G, l);
-        double ff;
-        const bool fired = out_step(st, A.c, G, s, &ff);
-        const unsigned om = __ballot_sync(kFull, fired) & 0x3FFu;
-        if (A.out.out_raster && lane == 0) A.out.out_raster[(size_t)img * N + s] = (uint16_t)om;
-        if (lane < kNO) {
-            if (A.out.ff) A.out.ff[((size_t)img * N + s) * kNO + lane] = ff;
-            if (A.out.v_out) A.out.v_out[((size_t)img * N + s) * kNO + lane] = st.v;
-        }
 #pragma unroll
-        for (int r = 0; r < kMaxVec; ++r) cur[r] = nxt[r];
+            for (int p = 0; p < 5; ++p) S.G[j * 5 + p] = g[p];
+        }
+        __syncwarp();
+        for (int j = 0; j < ns; ++j) {
+            const int s = s0 + j;
+            double ff;
+            out_step(st, A.c, Gd[j * kNO + l], s, l, &ff);
+            if (A.out.out_raster && lane == 0) A.out.out_raster[(size_t)img * N + s] = (uint16_t)st.prev;
+            if (lane < kNO) {
+                if (A.out.ff) A.out.ff[((size_t)img * N + s) * kNO + lane] = ff;
+                if (A.out.v_out) A.out.v_out[((size_t)img * N + s) * kNO + lane] = st.v;
+            }
+        }
+        __syncwarp();
     }
     if (lane < kNO) A.out.counts[(size_t)img * kNO + lane] = st.cnt;
 }

@@ -340,9 +340,8 @@ __global__ void __launch_bounds__(kTThreads) k_normad(const TrainArgs T, const N
             out_init(st, c);
             for (int s = 0; s < N; ++s) {
                 double ff;
-                const bool fired = out_step(st, c, GR[s * kNO + l], s, &ff);
-                const unsigned om = __ballot_sync(kFull, fired) & 0x3FFu;
-                if (lane == 0) OMASK[s] = (uint16_t)om;
+                out_step(st, c, GR[s * kNO + l], s, l, &ff);
+                if (lane == 0) OMASK[s] = (uint16_t)st.prev;
             }
             if (lane < kNO) T.counts[(size_t)i * kNO + lane] = st.cnt;
         }

@@ -38,11 +38,20 @@ int validate(const snn_consts_t *c) {
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// ---- inference workspace: tile_pos | n_tiles | tile_base | raster (upper bound)
+// The specialised kernel is exact for any bank whose taps EQUAL the default
+// ones (+0.0 and -0.0 zero taps are both skipped, see def_current).
+bool is_default_bank(const snn_consts_t &c) {
+    for (int f = 0; f < kNF; ++f)
+        for (int k = 0; k < 9; ++k)
+            if (!(c.taps[f][k] == def_tap(f, k))) return false;
+    return true;
+}
+
+// ---- inference workspace: tile_pos | n_tiles | tile_base | partials (upper bound)
 struct InferWS {
     uint16_t *tile_pos;
     int32_t *n_tiles, *tile_base;
-    uint8_t *raster;
+    double *partial;
 };
 
 size_t infer_ws_layout(const snn_consts_t *c, int64_t n, char *base, InferWS *w) {
@@ -56,7 +65,7 @@ size_t infer_ws_layout(const snn_consts_t *c, int64_t n, char *base, InferWS *w)
     x.tile_pos = (uint16_t *)take((size_t)n * kMaxTiles * kTile * 2);
     x.n_tiles = (int32_t *)take((size_t)n * 4);
     x.tile_base = (int32_t *)take((size_t)(n + 1) * 4);
-    x.raster = (uint8_t *)take((size_t)n * kMaxTiles * c->n_steps * kTile * 2);
+    x.partial = (double *)take((size_t)n * kMaxTiles * (is_default_bank(*c) ? 1 : 2) * c->n_steps * kNO * 8);
     if (w) *w = x;
     return off;
 }
@@ -110,6 +119,8 @@ size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base) 
     return off;
 }
 
+cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;  // snn_profile_events
+
 int sm_count() {
     static int sms = 0;
     if (!sms) {
@@ -122,29 +133,14 @@ int sm_count() {
 }
 
 // prep -> tile scan -> hidden (persistent) [-> output]; raster etc. in A
-// The specialised kernel is exact for any bank whose taps EQUAL the default
-// ones (+0.0 and -0.0 zero taps are both skipped, see def_current).
-bool is_default_bank(const snn_consts_t &c) {
-    for (int f = 0; f < kNF; ++f)
-        for (int k = 0; k < 9; ++k)
-            if (!(c.taps[f][k] == def_tap(f, k))) return false;
-    return true;
-}
-
-template <bool TRACE, bool DEF>
+template <bool TRACE, bool DEF, bool RASTER, bool GSUM>
 int launch_batch(const BatchArgs &A, bool with_output, cudaStream_t st) {
-    static int hid_blocks = 0, out_cfg = 0;
+    static int hid_blocks = 0;
     if (!hid_blocks) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hid_blocks, k_hidden<TRACE, DEF>, kThreads, 0) !=
-                cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hid_blocks, k_hidden<TRACE, DEF, RASTER, GSUM>, kThreads,
+                                                          0) != cudaSuccess ||
             hid_blocks <= 0)
             hid_blocks = 4;
-    }
-    if (!out_cfg) {
-        if (cudaFuncSetAttribute(k_output, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOutSmemBytes) !=
-            cudaSuccess)
-            return cuda_check("cudaFuncSetAttribute(k_output)");
-        out_cfg = 1;
     }
     int rc;
     const unsigned n = (unsigned)A.n_images;
@@ -154,8 +150,10 @@ int launch_batch(const BatchArgs &A, bool with_output, cudaStream_t st) {
     if ((rc = cuda_check("k_tile_scan"))) return rc;
     const int64_t max_groups = (2 * A.n_images * kMaxTiles + kWPC - 1) / kWPC;
     const unsigned grid = (unsigned)std::min<int64_t>((int64_t)hid_blocks * sm_count(), max_groups);
-    k_hidden<TRACE, DEF><<<grid, kThreads, 0, st>>>(A);
+    if (g_ev_before) cudaEventRecord(g_ev_before, st);
+    k_hidden<TRACE, DEF, RASTER, GSUM><<<grid, kThreads, 0, st>>>(A);
     if ((rc = cuda_check("k_hidden"))) return rc;
+    if (g_ev_after) cudaEventRecord(g_ev_after, st);
     if (with_output) {
         k_output<<<(n + kOutWarps - 1) / kOutWarps, kOutWarps * 32, kOutSmemBytes, st>>>(A);
         if ((rc = cuda_check("k_output"))) return rc;
@@ -180,6 +178,11 @@ NormadCaps normad_caps(const snn_consts_t *c) {
 }  // namespace
 
 extern "C" int snn_abi_version(void) { return SNN_ABI_VERSION; }
+
+extern "C" void snn_profile_events(void *before, void *after) {
+    g_ev_before = (cudaEvent_t)before;
+    g_ev_after = (cudaEvent_t)after;
+}
 extern "C" const char *snn_last_error(void) { return g_err; }
 
 extern "C" int snn_input_table(const snn_consts_t *c, double *d_ctab, uint8_t *d_spk, void *stream) {
@@ -222,11 +225,20 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
     A.tile_pos = out->tile_pos ? out->tile_pos : w.tile_pos;
     A.n_tiles = out->n_tiles ? out->n_tiles : w.n_tiles;
     A.tile_base = out->tile_base ? out->tile_base : w.tile_base;
-    A.raster = out->raster ? out->raster : w.raster;
+    A.raster = out->raster;
+    A.partial = w.partial;
     A.out = *out;
     const bool def = is_default_bank(*c);
-    if (out->v_hid) return def ? launch_batch<true, true>(A, true, s) : launch_batch<true, false>(A, true, s);
-    return def ? launch_batch<false, true>(A, true, s) : launch_batch<false, false>(A, true, s);
+    A.items_per_tile = def ? 1 : 2;
+    const bool raster = out->raster != nullptr;
+    if (out->v_hid) {
+        if (raster) return def ? launch_batch<true, true, true, true>(A, true, s)
+                               : launch_batch<true, false, true, true>(A, true, s);
+        return def ? launch_batch<true, true, false, true>(A, true, s) : launch_batch<true, false, false, true>(A, true, s);
+    }
+    if (raster) return def ? launch_batch<false, true, true, true>(A, true, s)
+                           : launch_batch<false, false, true, true>(A, true, s);
+    return def ? launch_batch<false, true, false, true>(A, true, s) : launch_batch<false, false, false, true>(A, true, s);
 }
 
 extern "C" size_t snn_train_workspace(const snn_consts_t *c, int64_t n) {
@@ -273,7 +285,9 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
         A.tile_pos = T.ws.tile_pos;
         A.n_tiles = T.ws.n_tiles;
         A.tile_base = T.ws.tile_base;
-        if ((rc = is_default_bank(*c) ? launch_batch<false, true>(A, false, s) : launch_batch<false, false>(A, false, s)))
+        A.items_per_tile = is_default_bank(*c) ? 1 : 2;
+        if ((rc = is_default_bank(*c) ? launch_batch<false, true, true, false>(A, false, s)
+                                      : launch_batch<false, false, true, false>(A, false, s)))
             return rc;
         T.n = cn;
         T.first = i0;

@@ -136,7 +136,7 @@ class Engine:
                 out["v_out"] = torch.empty((n, N, N_OUTPUTS), dtype=torch.float64, device=dev)
                 out["v_hid"] = torch.full((n, N, N_HIDDEN), float(c.lif_hid.el), dtype=torch.float64, device=dev)
         per_img = max(1, self.lib.snn_infer_workspace(ctypes.byref(c), 1))
-        chunk = max(1, min(n, (1 << 30) // per_img))
+        chunk = max(1, min(n, (4 << 30) // per_img))
         if max_chunk:
             chunk = min(chunk, max_chunk)
         if raster:
