@@ -213,44 +213,88 @@ __device__ __forceinline__ double def_current(const double (&x)[9]) {
     return I;
 }
 
-__device__ __forceinline__ void lif_update(double I, double &v, int &live_from, int s, int relive,
-                                           const snn_lif_t &ph, unsigned &m, int bit) {
-    const double cand = lif_candidate(v, I, ph);
-    const bool ok = s >= live_from;
-    const bool fired = ok && cand >= ph.vt;
-    v = ok ? (fired ? ph.el : cand) : v;
-    live_from = fired ? relive : live_from;
-    m |= (fired ? 1u : 0u) << bit;
+// One hidden LIF step (neurons.py:113-126).  Two exact identities keep it
+// short: a neuron that is not live has v == E_L (it was reset at its spike and
+// has been frozen since), so v' = (!live || fired || vn < E_L) ? E_L : vn; and
+// since threshold > rest (LifParams validation, neurons.py:39-47),
+// max(vn, E_L) >= V_T <=> vn >= V_T.  With SGN (E_L < 0 < V_T, the defaults)
+// both comparisons run on the integer pipe on the IEEE bit patterns, which
+// order like the values for these signs: vn >= V_T <=> (int64)bits(vn) >=
+// bits(V_T); vn < E_L <=> (uint64)bits(vn) > bits(E_L).  That leaves the FP64
+// pipe (this kernel's bound) with the five arithmetic ops only.
+struct LifK {
+    double g, el, beta, vt;
+    long long el_bits, vt_bits;
+};
+
+__device__ __forceinline__ LifK lif_k(const snn_lif_t &p) {
+    return LifK{p.g, p.el, p.beta, p.vt, __double_as_longlong(p.el), __double_as_longlong(p.vt)};
+}
+
+template <bool SGN>
+__device__ __forceinline__ void lif_update(double I, double &v, int &live_from, int s, int relive, const LifK &ph,
+                                           unsigned &m, int bit) {
+    double t = __dsub_rn(v, ph.el);
+    t = __dmul_rn(ph.g, t);
+    t = __dsub_rn(I, t);
+    t = __dmul_rn(ph.beta, t);
+    const double vn = __dadd_rn(v, t);
+    // pr: refractory (s < live_from); pf: fired = live && vn >= V_T;
+    // pz: frozen || fired || vn < E_L  ->  v = E_L, else v = vn.
+    if (SGN) {  // the threshold test on the integer pipe, the clamp test on the FP64 pipe
+        asm("{\n\t.reg .pred pr, pf, pa, pz;\n\t"
+            "setp.lt.s32 pr, %3, %1;\n\t"
+            "setp.ge.and.s64 pf, %5, %6, !pr;\n\t"
+            "or.pred pa, pr, pf;\n\t"
+            "setp.lt.or.f64 pz, %4, %7, pa;\n\t"
+            "selp.f64 %0, %7, %4, pz;\n\t"
+            "@pf mov.b32 %1, %8;\n\t"
+            "@pf or.b32 %2, %2, %9;\n\t}"
+            : "=d"(v), "+r"(live_from), "+r"(m)
+            : "r"(s), "d"(vn), "l"(__double_as_longlong(vn)), "l"(ph.vt_bits), "d"(ph.el), "r"(relive),
+              "r"(1u << bit));
+    } else {
+        asm("{\n\t.reg .pred pr, pf, pa, pz;\n\t"
+            "setp.lt.s32 pr, %3, %1;\n\t"
+            "setp.ge.and.f64 pf, %4, %5, !pr;\n\t"
+            "or.pred pa, pr, pf;\n\t"
+            "setp.lt.or.f64 pz, %4, %6, pa;\n\t"
+            "selp.f64 %0, %6, %4, pz;\n\t"
+            "@pf mov.b32 %1, %7;\n\t"
+            "@pf or.b32 %2, %2, %8;\n\t}"
+            : "=d"(v), "+r"(live_from), "+r"(m)
+            : "r"(s), "d"(vn), "d"(ph.vt), "d"(ph.el), "r"(relive), "r"(1u << bit));
+    }
 }
 
 // All 12 features of one lane with the default bank: 4 Sobel currents, their
 // exact negations (fma(x,-w,-a) == -fma(x,w,a) under round-to-nearest-even),
 // and 4 corner currents -- 60 FMAs instead of 108.
-__device__ __forceinline__ unsigned hidden_step_def(const snn_lif_t &ph, const double (&x)[9],
+template <bool SGN>
+__device__ __forceinline__ unsigned hidden_step_def(const LifK &ph, const double (&x)[9],
                                                     double (&v)[kNF], int (&live_from)[kNF], int s,
                                                     int relive) {
     unsigned m = 0;
     const double e0 = def_current<0>(x), e1 = def_current<1>(x), e2 = def_current<2>(x), e3 = def_current<3>(x);
-    lif_update(e0, v[0], live_from[0], s, relive, ph, m, 0);
-    lif_update(e1, v[1], live_from[1], s, relive, ph, m, 1);
-    lif_update(e2, v[2], live_from[2], s, relive, ph, m, 2);
-    lif_update(e3, v[3], live_from[3], s, relive, ph, m, 3);
-    lif_update(-e0, v[4], live_from[4], s, relive, ph, m, 4);
-    lif_update(-e1, v[5], live_from[5], s, relive, ph, m, 5);
-    lif_update(-e2, v[6], live_from[6], s, relive, ph, m, 6);
-    lif_update(-e3, v[7], live_from[7], s, relive, ph, m, 7);
-    lif_update(def_current<8>(x), v[8], live_from[8], s, relive, ph, m, 8);
-    lif_update(def_current<9>(x), v[9], live_from[9], s, relive, ph, m, 9);
-    lif_update(def_current<10>(x), v[10], live_from[10], s, relive, ph, m, 10);
-    lif_update(def_current<11>(x), v[11], live_from[11], s, relive, ph, m, 11);
+    lif_update<SGN>(e0, v[0], live_from[0], s, relive, ph, m, 0);
+    lif_update<SGN>(e1, v[1], live_from[1], s, relive, ph, m, 1);
+    lif_update<SGN>(e2, v[2], live_from[2], s, relive, ph, m, 2);
+    lif_update<SGN>(e3, v[3], live_from[3], s, relive, ph, m, 3);
+    lif_update<SGN>(-e0, v[4], live_from[4], s, relive, ph, m, 4);
+    lif_update<SGN>(-e1, v[5], live_from[5], s, relive, ph, m, 5);
+    lif_update<SGN>(-e2, v[6], live_from[6], s, relive, ph, m, 6);
+    lif_update<SGN>(-e3, v[7], live_from[7], s, relive, ph, m, 7);
+    lif_update<SGN>(def_current<8>(x), v[8], live_from[8], s, relive, ph, m, 8);
+    lif_update<SGN>(def_current<9>(x), v[9], live_from[9], s, relive, ph, m, 9);
+    lif_update<SGN>(def_current<10>(x), v[10], live_from[10], s, relive, ph, m, 10);
+    lif_update<SGN>(def_current<11>(x), v[11], live_from[11], s, relive, ph, m, 11);
     return m;
 }
 
 // Generic bank: one lane's 6 feature neurons (features H*6 .. H*6+5).
-template <int H>
-__device__ __forceinline__ unsigned hidden_step(const BatchArgs &A, const double (&x)[9], double (&v)[kNF],
-                                                int (&live_from)[kNF], int s, int relive) {
-    const snn_lif_t &ph = A.c.lif_hid;
+template <int H, bool SGN>
+__device__ __forceinline__ unsigned hidden_step(const BatchArgs &A, const LifK &ph, const double (&x)[9],
+                                                double (&v)[kNF], int (&live_from)[kNF], int s, int relive) {
     double I[kHalf];
 #pragma unroll
     for (int f = 0; f < kHalf; ++f) I[f] = __dmul_rn(x[0], A.c.taps[H * kHalf + f][0]);
@@ -260,7 +304,7 @@ __device__ __forceinline__ unsigned hidden_step(const BatchArgs &A, const double
         for (int f = 0; f < kHalf; ++f) I[f] = __fma_rn(x[k], A.c.taps[H * kHalf + f][k], I[f]);
     unsigned m = 0;
 #pragma unroll
-    for (int f = 0; f < kHalf; ++f) lif_update(I[f], v[f], live_from[f], s, relive, ph, m, f);
+    for (int f = 0; f < kHalf; ++f) lif_update<SGN>(I[f], v[f], live_from[f], s, relive, ph, m, f);
     return m;
 }
 
@@ -361,7 +405,7 @@ __device__ __forceinline__ void chunk_partials(const BatchArgs &A, uint16_t *ids
     }
 }
 
-template <bool TRACE, bool DEF, bool RASTER, bool GSUM>
+template <bool TRACE, bool DEF, bool RASTER, bool GSUM, bool SGN>
 __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
     __shared__ __align__(128) double s_tab[kStages][kChunk * 256];
     __shared__ uint64_t s_full[kStages];
@@ -391,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
     __syncthreads();
 
     const double el = A.c.lif_hid.el, refr = A.c.lif_hid.refr;
+    const LifK ph = lif_k(A.c.lif_hid);
     int64_t q = 0;
     for (int gi = 0; gi < my_groups; ++gi) {
         const int item = ((int)blockIdx.x + gi * (int)gridDim.x) * kWPC + warp;
@@ -454,9 +499,9 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
                     for (int k = 0; k < 9; ++k) x[k] = T[(lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu];
                     const int relive = next_live_step(s, refr);
                     unsigned m;
-                    if (DEF) m = hidden_step_def(A.c.lif_hid, x, v, live_from, s, relive);
-                    else m = half ? hidden_step<1>(A, x, v, live_from, s, relive)
-                                  : hidden_step<0>(A, x, v, live_from, s, relive);
+                    if (DEF) m = hidden_step_def<SGN>(ph, x, v, live_from, s, relive);
+                    else m = half ? hidden_step<1, SGN>(A, ph, x, v, live_from, s, relive)
+                                  : hidden_step<0, SGN>(A, ph, x, v, live_from, s, relive);
                     if (TRACE && on && A.out.v_hid) {
                         double *dst = A.out.v_hid + ((size_t)img * N + s) * kNH + pos * kNF + half * kHalf;
 #pragma unroll

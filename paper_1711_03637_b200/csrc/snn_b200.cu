@@ -47,6 +47,10 @@ bool is_default_bank(const snn_consts_t &c) {
     return true;
 }
 
+// Hidden-layer comparisons can run on the integer pipe when E_L < 0 < V_T
+// (see lif_update); any other sign pattern takes the FP64 compares.
+bool signed_lif(const snn_consts_t &c) { return c.lif_hid.el < 0.0 && c.lif_hid.vt > 0.0; }
+
 // ---- inference workspace: tile_pos | n_tiles | tile_base | partials (upper bound)
 struct InferWS {
     uint16_t *tile_pos;
@@ -133,12 +137,12 @@ int sm_count() {
 }
 
 // prep -> tile scan -> hidden (persistent) [-> output]; raster etc. in A
-template <bool TRACE, bool DEF, bool RASTER, bool GSUM>
+template <bool TRACE, bool DEF, bool RASTER, bool GSUM, bool SGN>
 int launch_batch(const BatchArgs &A, bool with_output, cudaStream_t st) {
     static int hid_blocks = 0;
     if (!hid_blocks) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hid_blocks, k_hidden<TRACE, DEF, RASTER, GSUM>, kThreads,
-                                                          0) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hid_blocks, k_hidden<TRACE, DEF, RASTER, GSUM, SGN>,
+                                                          kThreads, 0) != cudaSuccess ||
             hid_blocks <= 0)
             hid_blocks = 4;
     }
@@ -151,7 +155,7 @@ int launch_batch(const BatchArgs &A, bool with_output, cudaStream_t st) {
     const int64_t max_groups = (2 * A.n_images * kMaxTiles + kWPC - 1) / kWPC;
     const unsigned grid = (unsigned)std::min<int64_t>((int64_t)hid_blocks * sm_count(), max_groups);
     if (g_ev_before) cudaEventRecord(g_ev_before, st);
-    k_hidden<TRACE, DEF, RASTER, GSUM><<<grid, kThreads, 0, st>>>(A);
+    k_hidden<TRACE, DEF, RASTER, GSUM, SGN><<<grid, kThreads, 0, st>>>(A);
     if ((rc = cuda_check("k_hidden"))) return rc;
     if (g_ev_after) cudaEventRecord(g_ev_after, st);
     if (with_output) {
@@ -159,6 +163,13 @@ int launch_batch(const BatchArgs &A, bool with_output, cudaStream_t st) {
         if ((rc = cuda_check("k_output"))) return rc;
     }
     return SNN_OK;
+}
+
+// Picks the k_hidden instantiation: TRACE variants always use FP64 compares.
+template <bool DEF, bool RASTER, bool GSUM>
+int launch_fast(const BatchArgs &A, bool with_output, cudaStream_t st) {
+    return signed_lif(A.c) ? launch_batch<false, DEF, RASTER, GSUM, true>(A, with_output, st)
+                           : launch_batch<false, DEF, RASTER, GSUM, false>(A, with_output, st);
 }
 
 // Shared-memory caps of k_normad: as many active neurons / events as fit in
@@ -232,13 +243,13 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
     A.items_per_tile = def ? 1 : 2;
     const bool raster = out->raster != nullptr;
     if (out->v_hid) {
-        if (raster) return def ? launch_batch<true, true, true, true>(A, true, s)
-                               : launch_batch<true, false, true, true>(A, true, s);
-        return def ? launch_batch<true, true, false, true>(A, true, s) : launch_batch<true, false, false, true>(A, true, s);
+        if (raster) return def ? launch_batch<true, true, true, true, false>(A, true, s)
+                               : launch_batch<true, false, true, true, false>(A, true, s);
+        return def ? launch_batch<true, true, false, true, false>(A, true, s)
+                   : launch_batch<true, false, false, true, false>(A, true, s);
     }
-    if (raster) return def ? launch_batch<false, true, true, true>(A, true, s)
-                           : launch_batch<false, false, true, true>(A, true, s);
-    return def ? launch_batch<false, true, false, true>(A, true, s) : launch_batch<false, false, false, true>(A, true, s);
+    if (raster) return def ? launch_fast<true, true, true>(A, true, s) : launch_fast<false, true, true>(A, true, s);
+    return def ? launch_fast<true, false, true>(A, true, s) : launch_fast<false, false, true>(A, true, s);
 }
 
 extern "C" size_t snn_train_workspace(const snn_consts_t *c, int64_t n) {
@@ -286,8 +297,8 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
         A.n_tiles = T.ws.n_tiles;
         A.tile_base = T.ws.tile_base;
         A.items_per_tile = is_default_bank(*c) ? 1 : 2;
-        if ((rc = is_default_bank(*c) ? launch_batch<false, true, true, false>(A, false, s)
-                                      : launch_batch<false, false, true, false>(A, false, s)))
+        if ((rc = is_default_bank(*c) ? launch_fast<true, true, false>(A, false, s)
+                                      : launch_fast<false, true, false>(A, false, s)))
             return rc;
         T.n = cn;
         T.first = i0;
