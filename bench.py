@@ -46,7 +46,8 @@ F_TRAIN_PER_IMAGE = 162_240
 # (default filter bank): stencil = 8 chains (4 Sobel, 4 corner) with
 # 8 DMUL + 52 DFMA = 112 flop, Sobel negations are free; LIF = 12 x 5 flop.
 FLOP_PER_ACTIVE_POS_STEP = 112 + 12 * 5
-LAUNCHES_PER_CHUNK = 4   # k_prep, k_tile_scan, k_hidden, k_output
+LAUNCHES_PER_CHUNK = 5   # per sub-batch: k_prep, k_tile_scan, k_hidden, k_gsum, k_output
+PIPE_IMAGES = 0          # snn_set_pipeline sub-batch (library default: off)
 
 
 def log(*a):
@@ -277,12 +278,7 @@ def run_ours(args):
     eng.stream.synchronize()
     barrier()
 
-    step_ms, kern_ms, hid_ms = [], [], []
-    # CUDA events the library records around k_hidden (snn_profile_events)
-    ev_b, ev_a = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev_b.record(eng.stream)
-    ev_a.record(eng.stream)
-    eng.stream.synchronize()
+    step_ms, kern_ms = [], []
     with Clocks(local) as clk:
         torch.cuda.synchronize()
         barrier()
@@ -291,9 +287,7 @@ def run_ours(args):
                 flush.zero_()               # evict the 7.8 MB input set from the 126 MB L2
             e0, k1, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record(eng.stream)
-            eng.lib.snn_profile_events(ctypes.c_void_p(ev_b.cuda_event), ctypes.c_void_p(ev_a.cuda_event))
             out = eng.infer(c, d_img, d_w)["counts"]
-            eng.lib.snn_profile_events(None, None)
             k1.record(eng.stream)
             if world > 1:
                 with torch.cuda.stream(eng.stream):
@@ -302,11 +296,13 @@ def run_ours(args):
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
             kern_ms.append(e0.elapsed_time(k1))
-            hid_ms.append(ev_b.elapsed_time(ev_a))
         torch.cuda.synchronize()
         barrier()
     clocks = clk.summary()
-    tot_ms, ker_ms, hk_ms = max_over_ranks([sum(step_ms), sum(kern_ms), sum(hid_ms)])
+    tot_ms, ker_ms = max_over_ranks([sum(step_ms), sum(kern_ms)])
+    # roofline pass: k_hidden timed alone (one un-pipelined launch per call,
+    # CUDA events the library records around it on its stream)
+    hk_ms, call1_ms = kernel_alone_ms(eng, c, d_img, d_w, flush, args.steps)
     value = N_IMAGES * args.steps / (tot_ms / 1e3)
     counts_dev = out
     ref_prefix = None
@@ -334,8 +330,8 @@ def run_ours(args):
         act = active_positions(shard.reshape(-1, 28, 28))
         n_steps = c.n_steps
         assert chunks_per_step == 1, "k_hidden events time one launch per step"
-        launch_ms = hk_ms / args.steps                       # k_hidden alone (CUDA events)
-        call_ms = ker_ms / args.steps                        # whole snn_infer call (4 kernels)
+        launch_ms = hk_ms                                    # k_hidden alone (CUDA events)
+        call_ms = ker_ms / args.steps                        # whole (pipelined) snn_infer call
         exec_flop_launch = float(act.sum()) * n_steps * FLOP_PER_ACTIVE_POS_STEP
         achieved = exec_flop_launch / (launch_ms * 1e-3) / 1e12
         dense_tflops = (b - a) * F_INF_PER_STEP * n_steps / (ker_ms / args.steps * 1e-3) / 1e12
@@ -354,12 +350,12 @@ def run_ours(args):
             "gpu_launches": int(args.steps * launches_per_step),
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": f64, "unit": "TFLOP/s",
                          "frac": achieved / f64, "traffic": None,
-                         "kernel": "k_hidden<DEF,GSUM> (fused stencil + hidden LIF + per-tile event-driven "
-                                   "contraction partials), timed alone with CUDA events (snn_profile_events)",
+                         "kernel": "k_hidden<DEF> (fused input-table gather + 3x3 stencil + hidden LIF, "
+                                   "spike raster out), timed alone with CUDA events (snn_profile_events)",
                          "achieved_basis": f"executed fp64 flop: active windows x N x {FLOP_PER_ACTIVE_POS_STEP}",
                          "peak_source": "measured in this run: FP64 DFMA microbenchmark (libsnn_peaks.so); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
-                         "launch_ms": launch_ms, "call_ms": call_ms,
+                         "launch_ms": launch_ms, "call_ms": call_ms, "unpipelined_call_ms": call1_ms,
                          "call_achieved_tflops": exec_flop_launch / (call_ms * 1e-3) / 1e12,
                          "dense_equiv_tflops": dense_tflops,
                          "dense_equiv_basis": "SURVEY 8(d) F_inf = 389,516 flop per image-step",
@@ -370,13 +366,48 @@ def run_ours(args):
     # ---- NormAD training (single GPU, rank 0)
     if rank == 0 and not args.skip_train:
         line["train"] = bench_train(args, sd, eng, d, cfg, bank)
+    if rank == 0 and not args.skip_latency:
+        line["latency"] = bench_latency(sd, d, w_fix, bank)
     if rank == 0 and world == 1 and not args.skip_cpu:
         line["cpu_baseline"] = cpu_baseline(d, w_fix)
+    if rank == 0 and not args.skip_c5 and os.path.exists(os.path.join(ROOT, "data", "c5_workload.npz")):
+        line["full_pass"] = bench_c5(sd, eng, cfg, bank, line)
     if rank == 0:
         print(json.dumps(line), flush=True)
     barrier()
     if world > 1:
         dist.destroy_process_group()
+
+
+def kernel_alone_ms(eng, c, d_img, d_w, flush, steps):
+    """k_hidden alone: pipelining off (one k_hidden launch per call), CUDA
+    events recorded by the library around the launch (snn_profile_events);
+    returns (k_hidden ms, un-pipelined call ms), medians over `steps` calls."""
+    import torch
+    lib = eng.lib
+    lib.snn_set_pipeline(0, 0)
+    ev_b, ev_a = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_b.record(eng.stream)   # torch creates the CUDA events lazily, on first record
+    ev_a.record(eng.stream)
+    hk, call = [], []
+    try:
+        eng.infer(c, d_img, d_w)
+        for _ in range(max(3, steps)):
+            with torch.cuda.stream(eng.stream):
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(eng.stream)
+            lib.snn_profile_events(ctypes.c_void_p(ev_b.cuda_event), ctypes.c_void_p(ev_a.cuda_event))
+            eng.infer(c, d_img, d_w)
+            lib.snn_profile_events(None, None)
+            e1.record(eng.stream)
+            e1.synchronize()
+            hk.append(ev_b.elapsed_time(ev_a))
+            call.append(e0.elapsed_time(e1))
+    finally:
+        lib.snn_profile_events(None, None)
+        lib.snn_set_pipeline(PIPE_IMAGES, 0)
+    return statistics.median(hk), statistics.median(call)
 
 
 def bench_train(args, sd, eng, d, cfg, bank):
@@ -426,6 +457,99 @@ def bench_train(args, sd, eng, d, cfg, bank):
                              "sample": f"oracle.train_epoch on the first {k} images (1 core, as the reference)"}}
 
 
+def bench_c5(sd, eng, cfg, bank, line):
+    """BASELINE configs[4] / SURVEY 8(d) config 5: one NormAD pass over the
+    60,000 images of synthetic_dataset(6000, seed=4000) in
+    epoch_permutation(0, 0, 60000) order from zero weights, then evaluation of
+    the 10,000 images of synthetic_dataset(1000, seed=5000) -- device time of
+    the whole pass (one training call + one inference call), and end to end
+    through train_epoch + batch_counts with host arrays.  Checked against the
+    reference's own run of the same pass (tests/golden/c5_reference.npz)."""
+    import torch
+    from paper_1711_03637_b200.engine import make_consts
+    d5 = np.load(os.path.join(ROOT, "data", "c5_workload.npz"))
+    order = d5["order"]
+    tr = d5["train_images"][order]
+    lab = d5["train_labels"][order]
+    ev = d5["eval_images"]
+    learn = sd.LearnConfig()
+    ct, ci = make_consts(cfg, bank, learn), make_consts(cfg, bank)
+    with torch.cuda.stream(eng.stream):
+        d_tr = torch.from_numpy(tr.reshape(len(tr), -1).copy()).to(eng.device)
+        d_lab = torch.from_numpy(lab.astype(np.uint8)).to(eng.device)
+        d_ev = torch.from_numpy(ev.reshape(len(ev), -1).copy()).to(eng.device)
+        d_w = torch.zeros((8112, 10), dtype=torch.float64, device=eng.device)
+    eng.train(ct, d_tr[:1000], d_lab[:1000], d_w)          # warm-up (workspaces, tables)
+    eng.infer(ci, d_ev[:1000], d_w)
+    d_w.zero_()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record(eng.stream)
+    counts_tr, status = eng.train(ct, d_tr, d_lab, d_w)
+    e1.record(eng.stream)
+    counts_ev = eng.infer(ci, d_ev, d_w)["counts"]
+    e2.record(eng.stream)
+    e2.synchronize()
+    t_train, t_eval = e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3
+    w = d_w.cpu().numpy()
+    ctr, cev = counts_tr.cpu().numpy(), counts_ev.cpu().numpy()
+    n_tr, n_ev = len(tr), len(ev)
+    # end to end through the public API (host arrays in and out)
+    t0 = time.perf_counter()
+    w_api, stats = sd.train_epoch(tr, lab, sd.zero_weights(), bank, cfg, learn)
+    cev_api = sd.batch_counts(ev, w_api, bank, cfg)
+    e2e_s = time.perf_counter() - t0
+    out = {"metric": "full NormAD pass (60,000 train) + 10,000-image eval, images/s (1 GPU)",
+           "value": (n_tr + n_ev) / (t_train + t_eval), "unit": "images/s",
+           "train_images_per_s": n_tr / t_train, "eval_images_per_s": n_ev / t_eval,
+           "train_s": t_train, "eval_s": t_eval,
+           "e2e": {"value": (n_tr + n_ev) / e2e_s, "unit": "images/s", "api": "train_epoch + batch_counts (host numpy)"},
+           "train_errors": int(stats.n_errors),
+           "eval_accuracy": float((np.argmax(cev, axis=1) == d5["eval_labels"]).mean()),
+           "api_matches_device_run": bool(np.array_equal(w_api, w) and np.array_equal(cev_api, cev))}
+    gp = os.path.join(ROOT, "tests", "golden", "c5_reference.npz")
+    if os.path.exists(gp):
+        g = np.load(gp)
+        wr = g["w_after_60000"]
+        out["parity"] = {"w_rel_err_vs_reference_after_60000": float(np.abs(w - wr).max() / np.abs(wr).max()),
+                         "train_counts_identical_frac": float((ctr == g["train_counts"]).all(axis=1).mean()),
+                         "eval_counts_first500_identical": bool(np.array_equal(cev[:500], g["eval_counts_500"])),
+                         "reference_cpu_train_s_60000_build_box": float(g["train_seconds"])}
+    cb = line.get("train", {}).get("cpu_baseline", {}).get("value")
+    ci_ = line.get("cpu_baseline", {}).get("value")
+    if cb and ci_:
+        est = n_tr / cb + n_ev / ci_
+        out["cpu_baseline"] = {"value": (n_tr + n_ev) / est, "unit": "images/s", "cores": "1 (train) / all (eval)",
+                               "kind": "port", "sample": "extrapolated from the timed oracle samples above "
+                               "(train: 1 core, sequential as the reference; eval: all host cores)"}
+    return out
+
+
+def bench_latency(sd, d, w_fix, bank):
+    """BASELINE configs[3] / SURVEY 8(d) config 4: real-time batch-1 latency.
+    Each of the 500 preprocessed synthetic canvases goes through the public
+    run_presentation (host uint8 image + float64 weights in, int64 counts
+    out) at T = 75 ms, dt = 1 ms, timed per call on the host exactly as the
+    reference service times inference_ms (service.py:76-78)."""
+    import dataclasses
+    imgs = d["c4_images"]
+    cfg75 = dataclasses.replace(sd.NetworkConfig(), t=0.075)
+    for x in imgs[:20]:
+        sd.run_presentation(x, w_fix, bank, cfg75)
+    ms = []
+    for x in imgs:
+        t0 = time.perf_counter()
+        sd.run_presentation(x, w_fix, bank, cfg75)
+        ms.append((time.perf_counter() - t0) * 1e3)
+    ms = np.array(ms)
+    gold = np.load(os.path.join(ROOT, "tests", "golden", "reference_golden.npz"))["c4_counts_t75_100"]
+    same = all(np.array_equal(sd.run_presentation(imgs[i], w_fix, bank, cfg75), gold[i]) for i in range(len(gold)))
+    return {"metric": "batch-1 run_presentation latency, T=75 ms, dt=1 ms (500 synthetic canvases)",
+            "p50_ms": float(np.percentile(ms, 50)), "p99_ms": float(np.percentile(ms, 99)),
+            "mean_ms": float(ms.mean()), "max_ms": float(ms.max()), "budget_ms": 100.0,
+            "api": "run_presentation (host image + host float64 weights each call)",
+            "c4_first100_counts_equal_reference": bool(same)}
+
+
 def cpu_baseline(d, w):
     from oracle import snn_oracle as orc
     cores = host_cores()
@@ -448,6 +572,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--skip-train", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-latency", action="store_true")
+    ap.add_argument("--skip-c5", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -40,6 +40,7 @@ extern "C" {
 #define SNN_N_OUTPUTS 10
 #define SNN_TILE 32          /* window positions per warp tile */
 #define SNN_MAX_TILES 22     /* ceil(676 / 32) */
+#define SNN_RASTER_CHUNK 8   /* steps per raster chunk (512 bytes per tile) */
 
 /* status codes (int return values and d_status[0]) */
 #define SNN_OK 0
@@ -77,11 +78,12 @@ typedef struct snn_consts {
 } snn_consts_t;
 
 /* Optional outputs of snn_infer; every pointer may be NULL except counts.
- * The hidden spike raster is compact: image i owns the block that starts at
- * byte tile_base[i] * N * 64 and is laid out [step][tile][half][lane]; each
- * byte is the 6-bit spike mask of features half*6 .. half*6+5 of the lane's
- * window (tile_pos).  A raster buffer must hold n * 22 * N * 64 bytes (the
- * upper bound). */
+ * The hidden spike raster is compact and chunked by 8 steps: with
+ * C = ceil(N / 8), image i owns the block that starts at byte
+ * tile_base[i] * C * 512, laid out [chunk][tile][half][lane][8 steps]; the
+ * byte for step chunk*8 + j is the 6-bit spike mask of features
+ * half*6 .. half*6+5 of the lane's window (tile_pos); steps >= N read 0.
+ * A raster buffer must hold n * 22 * C * 512 bytes (the upper bound). */
 typedef struct snn_infer_out {
     int32_t *counts;     /* [n][10] output spike counts */
     uint8_t *raster;     /* compact hidden raster (see above) */
@@ -117,6 +119,14 @@ int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t n_images,
  * kernel (k_hidden) and `after` just after it, so a caller can time that
  * kernel alone with cudaEventElapsedTime.  Pass NULLs to disable. */
 void snn_profile_events(void *before, void *after);
+
+/* Tuning of snn_infer: calls with more than images_per_subbatch images (and
+ * no caller-visible raster) are pipelined in sub-batches -- the hidden layer
+ * of one sub-batch overlaps the contraction and output layer of the previous
+ * one on an internal stream; 0 disables.  hidden_ctas_per_sm caps the
+ * persistent k_hidden grid (0 = occupancy limit).  Defaults: 0, 0 (measured:
+ * no gain on one B200 -- the persistent k_hidden leaves no room to overlap). */
+void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_per_sm);
 
 /* Bytes of device workspace snn_train needs for n images. */
 size_t snn_train_workspace(const snn_consts_t *c, int64_t n_images);

@@ -19,6 +19,12 @@ SNN_ECUDA = 1002
 
 MAX_TILES = 22
 TILE = 32
+RASTER_CHUNK = 8
+
+
+def raster_bytes(n_images: int, n_steps: int) -> int:
+    """Upper bound of the compact hidden raster of n images (include/snn_b200.h)."""
+    return n_images * MAX_TILES * (-(-n_steps // RASTER_CHUNK)) * 2 * TILE * RASTER_CHUNK
 
 _d = ctypes.c_double
 _vp = ctypes.c_void_p
@@ -63,6 +69,7 @@ SIGNATURES = [
     ("snn_infer", ctypes.c_int, [ctypes.POINTER(ConstsC), _vp, ctypes.c_int64, _vp, _vp,
                                  ctypes.POINTER(InferOutC), _vp, ctypes.c_size_t, _vp]),
     ("snn_profile_events", None, [_vp, _vp]),
+    ("snn_set_pipeline", None, [ctypes.c_int64, ctypes.c_int]),
     ("snn_train_workspace", ctypes.c_size_t, [ctypes.POINTER(ConstsC), ctypes.c_int64]),
     ("snn_train", ctypes.c_int, [ctypes.POINTER(ConstsC), _vp, _vp, ctypes.c_int64, _vp, _vp, _vp,
                                  _vp, _vp, ctypes.c_size_t, _vp]),

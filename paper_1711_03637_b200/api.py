@@ -63,13 +63,16 @@ def _fetch(eng, t) -> np.ndarray:
 def decode_hidden(raster: np.ndarray, tile_base: int, tile_pos: np.ndarray, n_tiles: int,
                   n_steps: int) -> np.ndarray:
     """Compact raster block of one image -> (N, 8112) bool hidden spike raster.
-    Layout (include/snn_b200.h): bytes [tile_base*N*64 ...), [step][tile][half][lane],
-    6-bit masks of features half*6 .. half*6+5 of the lane's window."""
+    Layout (include/snn_b200.h): C = ceil(N/8) chunks, bytes
+    [tile_base*C*512 ...), [chunk][tile][half][lane][8 steps], 6-bit masks of
+    features half*6 .. half*6+5 of the lane's window."""
     out = np.zeros((n_steps, N_HIDDEN), dtype=bool)
     if n_tiles == 0:
         return out
-    blk = raster[tile_base * n_steps * 64:(tile_base + n_tiles) * n_steps * 64]
-    blk = blk.reshape(n_steps, n_tiles, 2, 32).astype(np.int64)
+    nch = -(-n_steps // 8)
+    blk = raster[tile_base * nch * 512:(tile_base + n_tiles) * nch * 512]
+    blk = blk.reshape(nch, n_tiles, 2, 32, 8).astype(np.int64)
+    blk = blk.transpose(0, 4, 1, 2, 3).reshape(nch * 8, n_tiles, 2, 32)[:n_steps]
     masks = blk[:, :, 0, :] | (blk[:, :, 1, :] << 6)              # (N, t, 32) 12-bit
     pos = tile_pos[:n_tiles].astype(np.int64) & 0xFFFF            # (t, 32)
     valid = pos != 0xFFFF

@@ -20,15 +20,17 @@
 //                registers for the whole trial).  The input-trace table is
 //                streamed through a 2-stage shared-memory ring by TMA bulk
 //                copies.  The stencil is the k-ordered FMA chain OpenBLAS uses
-//                for np.tensordot, so currents are bit-identical.  Output: one
-//                12-bit spike mask per lane and step (the raster).
+//                for np.tensordot, so currents are bit-identical.  Output: the
+//                spike raster, 6-bit masks per lane, step and feature half,
+//                stored once per 8-step chunk (two 8-byte stores per lane).
 //   k_output     one warp per image.  c_hidden @ W is event-driven: every
 //                hidden kernel trace is a linear recursion in its own spikes,
 //                so sum_k c_k(n) W[k,l] = A_l(n) - B_l(n) with
 //                A_l(n) = A_l(n-1) e^{-dt/t1} + G_l(n), G_l(n) = sum of the W
-//                rows of the neurons spiking at n.  The warp gathers those W
-//                rows with cp.async (a whole batch in flight), sums them in
-//                ascending neuron order and runs the 10-neuron output layer.
+//                rows of the neurons spiking at n.  Per chunk the warp turns
+//                the raster into per-step spike lists (ascending neuron id),
+//                sums the W rows of each list in that order and runs the
+//                10-neuron output layer.
 // Every reduction has a fixed order: results are deterministic run to run.
 #pragma once
 #include "snn_common.cuh"
@@ -43,11 +45,16 @@ constexpr int kOutWarps = 4;     // images per k_output CTA (one warp each)
 
 constexpr int kHalf = kNF / 2;   // features per k_hidden work item
 
-// Raster layout (bytes): image i owns the block starting at tile_base[i]*N*64,
-// laid out [step][tile][half][lane]; each byte is the 6-bit spike mask of
-// features half*6 .. half*6+5 of the lane's window.
-__host__ __device__ inline size_t raster_at(int64_t tile_base_img, int N, int ntiles, int s, int t) {
-    return ((size_t)tile_base_img * N + (size_t)s * ntiles + t) * (2 * kTile);
+// Raster layout (bytes; include/snn_b200.h): image i owns the block starting at
+// tile_base[i] * nchunks * 512, laid out [chunk][tile][half][lane][8 steps];
+// each byte is the 6-bit spike mask of features half*6 .. half*6+5 of the
+// lane's window at step chunk*8 + j (0 past the last step).
+constexpr int kRastTC = 2 * kTile * kChunk;  // 512 bytes per (tile, chunk)
+
+__host__ __device__ inline int n_chunks(int N) { return (N + kChunk - 1) / kChunk; }
+
+__host__ __device__ inline size_t raster_tc(int64_t tile_base_img, int nchunks, int ntiles, int ch, int t) {
+    return ((size_t)tile_base_img * nchunks + (size_t)ch * ntiles + t) * kRastTC;
 }
 
 struct BatchArgs {
@@ -59,8 +66,7 @@ struct BatchArgs {
     uint16_t *tile_pos;      // [n][22][32] window of each lane, 0xFFFF = none
     int32_t *n_tiles;        // [n]
     int32_t *tile_base;      // [n+1] exclusive prefix of n_tiles
-    uint8_t *raster;         // sum(n_tiles) * N * 64 spike-mask bytes (see raster_at)
-    double *partial;         // [items][N][10] per-item G partials (inference)
+    uint8_t *raster;         // sum(n_tiles) * nchunks * 512 spike-mask bytes (see raster_tc)
     int32_t items_per_tile;  // 1 (default bank) or 2 (generic bank)
     snn_infer_out_t out;     // counts / out_raster / ff / v_out / v_hid
 };
@@ -314,102 +320,10 @@ __device__ __forceinline__ unsigned hidden_step(const BatchArgs &A, const LifK &
 // features, which keeps the 54 runtime taps of a warp within the register
 // budget.  The table chunks form one continuous stream across groups, so the
 // TMA ring never drains between groups.
-// Per-item partial of G for the steps of one chunk: G_item(s, l) = sum of
-// W[k, l] over the item's neurons k spiking at s, in (lane, feature) order.
-// One packed warp scan lists the ids of all 8 steps; then lane (j, q) sums
-// step j's rows for outputs q, q+4, q+8 sequentially in list order (fixed
-// order: deterministic).  Done at the chunk end so the W loads of 8 steps
-// overlap other warps' FP64 work; an item's ~46 spiking neurons keep their W
-// rows in L1.
-constexpr int kPIds = 256;  // ids per chunk staged in shared memory
-
-__device__ __forceinline__ void chunk_partials(const BatchArgs &A, uint16_t *ids, int item, int s0, int nrows,
-                                               uint64_t mlo, uint64_t mhi, int id0) {
-    const int lane = threadIdx.x & 31;
-    const int N = A.c.n_steps;
-    double *P = A.partial + (size_t)item * N * kNO;
-    uint64_t cA = 0, cB = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        cA |= (uint64_t)__popc((unsigned)(mlo >> (16 * q)) & 0xFFFFu) << (16 * q);
-        cB |= (uint64_t)__popc((unsigned)(mhi >> (16 * q)) & 0xFFFFu) << (16 * q);
-    }
-    uint64_t tA, tB;
-    const uint64_t eA = warp_excl_scan_u64(cA, &tA), eB = warp_excl_scan_u64(cB, &tB);
-    int base[kChunk + 1];
-    base[0] = 0;
-#pragma unroll
-    for (int j = 0; j < kChunk; ++j)
-        base[j + 1] = base[j] + (int)(((j < 4 ? tA : tB) >> (16 * (j & 3))) & 0xFFFF);
-    const int total = base[kChunk];
-    const int jj = lane >> 2, q = lane & 3;  // lane -> (step jj, outputs q, q+4, q+8)
-    if (total <= kPIds) {
-        if (total) {
-#pragma unroll
-            for (int j = 0; j < kChunk; ++j) {
-                unsigned mm = (unsigned)((j < 4 ? mlo : mhi) >> (16 * (j & 3))) & 0xFFFFu;
-                int k = base[j] + (int)(((j < 4 ? eA : eB) >> (16 * (j & 3))) & 0xFFFF);
-                while (mm) {
-                    const int f = __ffs(mm) - 1;
-                    mm &= mm - 1;
-                    ids[k++] = (uint16_t)(id0 + f);
-                }
-            }
-        }
-        __syncwarp();
-        if (jj < nrows) {
-            int lo = 0, hi = 0;
-#pragma unroll
-            for (int j = 0; j < kChunk; ++j)
-                if (j == jj) {
-                    lo = base[j];
-                    hi = base[j + 1];
-                }
-            double g0 = 0.0, g1 = 0.0, g2 = 0.0;
-            for (int e = lo; e < hi; ++e) {
-                const double *row = A.w + (size_t)ids[e] * kNO;
-                g0 = __dadd_rn(g0, __ldg(row + q));
-                g1 = __dadd_rn(g1, __ldg(row + q + 4));
-                if (q < 2) g2 = __dadd_rn(g2, __ldg(row + q + 8));
-            }
-            double *dst = P + (size_t)(s0 + jj) * kNO;
-            dst[q] = g0;
-            dst[q + 4] = g1;
-            if (q < 2) dst[q + 8] = g2;
-        }
-        __syncwarp();
-        return;
-    }
-    // rare: more than kPIds spikes in one chunk of one item -- one step at a time, in windows
-    for (int j = 0; j < nrows; ++j) {
-        const unsigned m = (unsigned)((j < 4 ? mlo : mhi) >> (16 * (j & 3))) & 0xFFFFu;
-        int tot;
-        const int off = warp_excl_scan_int(__popc(m), &tot);
-        double g[3] = {0.0, 0.0, 0.0};
-        for (int w0 = 0; w0 < tot; w0 += kPIds) {
-            const int wn = min(kPIds, tot - w0);
-            int k = off - w0;
-            unsigned mm = m;
-            while (mm) {
-                const int f = __ffs(mm) - 1;
-                mm &= mm - 1;
-                if (k >= 0 && k < wn) ids[k] = (uint16_t)(id0 + f);
-                ++k;
-            }
-            __syncwarp();
-            if (lane < kNO)
-                for (int e = 0; e < wn; ++e) g[0] = __dadd_rn(g[0], __ldg(A.w + (size_t)ids[e] * kNO + lane));
-            __syncwarp();
-        }
-        if (lane < kNO) P[(size_t)(s0 + j) * kNO + lane] = g[0];
-    }
-}
-
-template <bool TRACE, bool DEF, bool RASTER, bool GSUM, bool SGN>
+template <bool TRACE, bool DEF, bool SGN>
 __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
     __shared__ __align__(128) double s_tab[kStages][kChunk * 256];
     __shared__ uint64_t s_full[kStages];
-    __shared__ uint16_t s_ids[kWPC][kPIds];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = A.c.n_steps;
     const int nchunks = (N + kChunk - 1) / kChunk;
@@ -478,10 +392,10 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
             v[f] = el;
             live_from[f] = 0;
         }
-        uint8_t *rout = (RASTER && live) ? A.raster + raster_at(A.tile_base[img], N, nt, 0, tile) + half * kTile + lane
-                                         : nullptr;
-        const size_t rstride = (size_t)nt * 2 * kTile;
-        const int id0 = pos * kNF + half * kHalf;
+        uint8_t *rout = live ? A.raster + raster_tc(A.tile_base[img], nchunks, nt, 0, tile) + half * (kRastTC / 2) +
+                                   lane * kChunk
+                             : nullptr;
+        const size_t rstride = (size_t)nt * kRastTC;  // one chunk of this image
 
         for (int ch = 0; ch < nchunks; ++ch, ++q) {
             const int b = (int)(q % kStages);
@@ -489,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
             const int nrows = min(kChunk, N - s0);
             if (live) {
                 mbar_wait(&s_full[b], (uint32_t)((q / kStages) & 1));
-                uint64_t mlo = 0, mhi = 0;  // the chunk's spike masks (16 bits per step)
+                uint64_t p0 = 0, p1 = 0;  // the chunk's 6-bit masks, one byte per step
 #pragma unroll 1
                 for (int j = 0; j < nrows; ++j) {
                     const int s = s0 + j;
@@ -507,17 +421,12 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
 #pragma unroll
                         for (int f = 0; f < (DEF ? kNF : kHalf); ++f) dst[f] = v[f];
                     }
-                    if (RASTER) {
-                        rout[(size_t)s * rstride] = (uint8_t)(m & 0x3Fu);
-                        if (DEF) rout[(size_t)s * rstride + kTile] = (uint8_t)(m >> kHalf);
-                    }
-                    if (GSUM) {
-                        const unsigned mo = on ? m : 0u;
-                        if (j < 4) mlo |= (uint64_t)mo << (16 * j);
-                        else mhi |= (uint64_t)mo << (16 * (j - 4));
-                    }
+                    p0 |= (uint64_t)(m & 0x3Fu) << (8 * j);
+                    if (DEF) p1 |= (uint64_t)(m >> kHalf) << (8 * j);
                 }
-                if (GSUM) chunk_partials(A, s_ids[warp], item, s0, nrows, mlo, mhi, id0);
+                uint64_t *dst = reinterpret_cast<uint64_t *>(rout + (size_t)ch * rstride);
+                dst[0] = p0;
+                if (DEF) dst[kTile] = p1;  // the second half plane, 256 bytes on
             }
             __syncthreads();  // every warp is done with stage b
             if (tid == 0 && q + kStages < stream_len) issue(q + kStages);
@@ -579,55 +488,232 @@ __device__ __forceinline__ bool out_step(OutState &st, const snn_consts_t &c, do
 }
 
 // ---------------------------------------------------------------------------
-// k_output: one warp per image -- G(s) = sum of the image's item partials in
-// item order, then the output layer.  For up to kOSteps steps at a time, lane
-// i computes G for steps i, i+32, ... (all 10 outputs, 80-byte partial rows
-// as double2 loads, all independent) into shared memory; then lanes 0..9 run
-// the sequential output layer from shared memory.
-constexpr int kOItems = 2 * kMaxTiles;
-constexpr int kOSteps = 96;
+// k_gsum: G(s, l) = sum of W[k, l] over the hidden neurons k spiking at step
+// s (network.py:311 restated event-driven), summed in ascending k -- a fixed
+// order, so results never depend on the batch an image is in.  One warp per
+// (image, 8-step chunk); chunks are independent, so a single image spreads
+// over ceil(N/8) warps.
+//   lists  per tile (in order): each lane counts its window's spikes per step;
+//          one packed warp scan gives per-lane offsets (8-bit fields when the
+//          tile-chunk has at most 255 spikes, else 16-bit).  Then the warp
+//          fills the tile's list slots 32 at a time: slot -> step (prefix of
+//          step totals) -> owning lane (binary search over the offsets in
+//          shared memory) -> bit of that lane's mask.  No divergent loops.
+//          Tiles ascend in window position, lanes within a tile too and
+//          features within a lane: every step list is in ascending neuron id.
+//   sums   lane (j, p) walks step j's list for outputs 2p, 2p+1 (16-byte W
+//          loads, 8 in flight).  A step with more than kStepCap spikes is
+//          summed afterwards tile by tile, in the same order.
+constexpr int kStepCap = 256;
+constexpr int kGWarps = 4;
 
-struct OutSmem {
-    double2 G[kOSteps * 5];
+__device__ __forceinline__ uint32_t byte_popc(uint32_t x) {  // popcount of each byte
+    x = x - ((x >> 1) & 0x55555555u);
+    x = (x & 0x33333333u) + ((x >> 2) & 0x33333333u);
+    return (x + (x >> 4)) & 0x0F0F0F0Fu;
+}
+
+// 12-bit mask of chunk step j from the two 6-bit planes
+__device__ __forceinline__ unsigned chunk_mask(uint64_t p0, uint64_t p1, int j) {
+    return (unsigned)((p0 >> (8 * j)) & 0x3Fu) | ((unsigned)((p1 >> (8 * j)) & 0x3Fu) << kHalf);
+}
+
+__device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+struct GsumSmem {
+    uint16_t ids[kChunk * kStepCap];  // the chunk's step lists
+    uint16_t pos[kMaxTiles * kTile];  // window position of each (tile, lane)
+    uint16_t off[kTile * kChunk];     // [lane][step] exclusive offsets within the tile
+    uint16_t msk[kTile * kChunk];     // [lane][step] 12-bit spike masks
 };
 
-__global__ void __launch_bounds__(kOutWarps * 32) k_output(const BatchArgs A) {
-    extern __shared__ __align__(16) uint8_t osmem[];
+__global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double *G) {
+    __shared__ __align__(16) GsumSmem smem[kGWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    OutSmem &S = reinterpret_cast<OutSmem *>(osmem)[warp];
-    const int64_t img = (int64_t)blockIdx.x * kOutWarps + warp;
+    GsumSmem &S = smem[warp];
+    const int N = A.c.n_steps, nch = n_chunks(N);
+    const int64_t task = (int64_t)blockIdx.x * kGWarps + warp;
+    if (task >= A.n_images * nch) return;
+    const int64_t img = task / nch;
+    const int ch = (int)(task - img * nch);
+    const int s0 = ch * kChunk, ns = min(kChunk, N - s0);
+    const int nt = A.n_tiles[img];
+    for (int k = lane; k < nt * kTile; k += 32) S.pos[k] = A.tile_pos[img * (kMaxTiles * kTile) + k];
+    const uint8_t *R = A.raster + raster_tc(A.tile_base[img], nch, nt, ch, 0) + lane * kChunk;
+    const double *W = A.w;
+    uint32_t run[kChunk];  // list lengths so far (warp-uniform)
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) run[j] = 0;
+    // the next tile's masks are loaded while this tile's list is built
+    uint2 n0 = make_uint2(0, 0), n1 = make_uint2(0, 0);
+    if (nt > 0) {
+        n0 = __ldcs(reinterpret_cast<const uint2 *>(R));
+        n1 = __ldcs(reinterpret_cast<const uint2 *>(R + kRastTC / 2));
+    }
+    __syncwarp();
+    for (int t = 0; t < nt; ++t) {
+        const uint2 a0 = n0, a1 = n1;
+        if (t + 1 < nt) {
+            const uint8_t *nxt = R + (size_t)(t + 1) * kRastTC;
+            n0 = __ldcs(reinterpret_cast<const uint2 *>(nxt));
+            n1 = __ldcs(reinterpret_cast<const uint2 *>(nxt + kRastTC / 2));
+        }
+        const uint32_t clo = byte_popc(a0.x) + byte_popc(a1.x);  // steps 0..3, one byte each (<= 12)
+        const uint32_t chi = byte_popc(a0.y) + byte_popc(a1.y);  // steps 4..7
+        const unsigned tot = __reduce_add_sync(kFull, ((clo * 0x01010101u) >> 24) + ((chi * 0x01010101u) >> 24));
+        if (tot == 0) continue;  // warp-uniform: no spike in this tile-chunk
+        uint4 ow, tw;            // exclusive offsets / tile totals, 16-bit fields, steps (0,1) (2,3) (4,5) (6,7)
+        if (tot <= 255) {        // one scan: 8-bit fields cannot overflow
+            const uint64_t c8 = ((uint64_t)chi << 32) | clo;
+            const uint64_t inc = warp_incl_scan_u64(c8);
+            const uint64_t exc = inc - c8;
+            const uint64_t tt = __shfl_sync(kFull, inc, 31);
+            ow = make_uint4(__byte_perm((uint32_t)exc, 0, 0x4140), __byte_perm((uint32_t)exc, 0, 0x4342),
+                            __byte_perm((uint32_t)(exc >> 32), 0, 0x4140), __byte_perm((uint32_t)(exc >> 32), 0, 0x4342));
+            tw = make_uint4(__byte_perm((uint32_t)tt, 0, 0x4140), __byte_perm((uint32_t)tt, 0, 0x4342),
+                            __byte_perm((uint32_t)(tt >> 32), 0, 0x4140), __byte_perm((uint32_t)(tt >> 32), 0, 0x4342));
+        } else {
+            const uint64_t cA = ((uint64_t)__byte_perm(clo, 0, 0x4342) << 32) | __byte_perm(clo, 0, 0x4140);
+            const uint64_t cB = ((uint64_t)__byte_perm(chi, 0, 0x4342) << 32) | __byte_perm(chi, 0, 0x4140);
+            const uint64_t iA = warp_incl_scan_u64(cA), iB = warp_incl_scan_u64(cB);
+            const uint64_t eA = iA - cA, eB = iB - cB;
+            const uint64_t tA = __shfl_sync(kFull, iA, 31), tB = __shfl_sync(kFull, iB, 31);
+            ow = make_uint4((uint32_t)eA, (uint32_t)(eA >> 32), (uint32_t)eB, (uint32_t)(eB >> 32));
+            tw = make_uint4((uint32_t)tA, (uint32_t)(tA >> 32), (uint32_t)tB, (uint32_t)(tB >> 32));
+        }
+        reinterpret_cast<uint4 *>(S.off)[lane] = ow;
+        reinterpret_cast<uint4 *>(S.msk)[lane] =
+            make_uint4(__byte_perm(a0.x, 0, 0x4140) | (__byte_perm(a1.x, 0, 0x4140) << kHalf),
+                       __byte_perm(a0.x, 0, 0x4342) | (__byte_perm(a1.x, 0, 0x4342) << kHalf),
+                       __byte_perm(a0.y, 0, 0x4140) | (__byte_perm(a1.y, 0, 0x4140) << kHalf),
+                       __byte_perm(a0.y, 0, 0x4342) | (__byte_perm(a1.y, 0, 0x4342) << kHalf));
+        const uint32_t T[kChunk] = {tw.x & 0xFFFFu, tw.x >> 16, tw.y & 0xFFFFu, tw.y >> 16,
+                                    tw.z & 0xFFFFu, tw.z >> 16, tw.w & 0xFFFFu, tw.w >> 16};
+        __syncwarp();
+        for (unsigned k0 = 0; k0 < tot; k0 += 32) {
+            const unsigned k = k0 + lane;
+            if (k < tot) {
+                // step of slot k: steps are laid out one after another
+                int j = 0;
+                unsigned sj = 0, acc = 0, base = run[0];
+#pragma unroll
+                for (int jj = 0; jj < kChunk; ++jj) {
+                    if (k >= acc) {
+                        j = jj;
+                        sj = acc;
+                        base = run[jj];
+                    }
+                    acc += T[jj];
+                }
+                const unsigned q = k - sj;  // rank within the tile's step-j list
+                int L = 0;                  // owning lane: largest L with off[L][j] <= q
+#pragma unroll
+                for (int st = 16; st > 0; st >>= 1)
+                    if (S.off[(L + st) * kChunk + j] <= q) L += st;
+                unsigned m = S.msk[L * kChunk + j];
+                for (unsigned r = q - S.off[L * kChunk + j]; r; --r) m &= m - 1u;
+                const unsigned slot = base + q;
+                if (slot < kStepCap) S.ids[j * kStepCap + slot] = (uint16_t)(S.pos[t * kTile + L] * kNF + __ffs(m) - 1);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) run[j] += T[j];
+        __syncwarp();
+    }
+    // ---- sums: lane (j, p) -> G[j][2p], G[j][2p+1]; rounds of 6 steps
+    double *Gi = G + ((size_t)img * N + s0) * kNO;
+#pragma unroll 1
+    for (int j0 = 0; j0 < ns; j0 += 6) {
+        const int j = j0 + lane / 5, p = lane % 5;
+        unsigned cnt = 0;
+#pragma unroll
+        for (int jj = 0; jj < kChunk; ++jj) cnt = jj == j ? run[jj] : cnt;
+        if (lane < 30 && j < ns && cnt <= kStepCap) {
+            const uint16_t *lst = S.ids + j * kStepCap;
+            const double2 *W2 = reinterpret_cast<const double2 *>(W) + p;
+            double g0 = 0.0, g1 = 0.0;
+            unsigned e = 0;
+            for (; e + 8 <= cnt; e += 8) {
+                double2 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldg(W2 + (size_t)lst[e + u] * (kNO / 2));
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    g0 = __dadd_rn(g0, v[u].x);
+                    g1 = __dadd_rn(g1, v[u].y);
+                }
+            }
+            for (; e < cnt; ++e) {
+                const double2 v = __ldg(W2 + (size_t)lst[e] * (kNO / 2));
+                g0 = __dadd_rn(g0, v.x);
+                g1 = __dadd_rn(g1, v.y);
+            }
+            reinterpret_cast<double2 *>(Gi + (size_t)j * kNO)[p] = make_double2(g0, g1);
+        }
+    }
+    // rare: a step with more than kStepCap spikes -- same order, tile by tile
+#pragma unroll 1
+    for (int j = 0; j < ns; ++j) {
+        unsigned cnt = 0;
+#pragma unroll
+        for (int jj = 0; jj < kChunk; ++jj) cnt = jj == j ? run[jj] : cnt;
+        if (cnt <= kStepCap) continue;  // warp-uniform
+        __syncwarp();
+        double g = 0.0;
+        for (int t = 0; t < nt; ++t) {
+            const uint8_t *src = R + (size_t)t * kRastTC;
+            unsigned m = chunk_mask(__ldcs(reinterpret_cast<const unsigned long long *>(src)),
+                                    __ldcs(reinterpret_cast<const unsigned long long *>(src + kRastTC / 2)), j);
+            int tt;
+            int k = warp_excl_scan_int(__popc(m), &tt);
+            const int id0 = (int)S.pos[t * kTile + lane] * kNF;
+            while (m) {
+                const int f = __ffs(m) - 1;
+                m &= m - 1u;
+                S.ids[k++] = (uint16_t)(id0 + f);
+            }
+            __syncwarp();
+            if (lane < kNO)
+                for (int e = 0; e < tt; ++e) g = __dadd_rn(g, __ldg(W + (size_t)S.ids[e] * kNO + lane));
+            __syncwarp();
+        }
+        if (lane < kNO) Gi[(size_t)j * kNO + lane] = g;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_output: the 10-neuron output layer (network.py:308-314), one warp per
+// image over its G rows (staged in shared memory kOSteps steps at a time).
+constexpr int kOSteps = 96;
+constexpr int kOutWarps2 = 4;
+
+__global__ void __launch_bounds__(kOutWarps2 * 32) k_output(const BatchArgs A, const double *G) {
+    __shared__ __align__(16) double s_g[kOutWarps2][kOSteps * kNO];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t img = (int64_t)blockIdx.x * kOutWarps2 + warp;
     if (img >= A.n_images) return;
     const int N = A.c.n_steps;
-    const int ni = A.n_tiles[img] * A.items_per_tile;
     const int l = lane < kNO ? lane : kNO - 1;
-    const double2 *P = reinterpret_cast<const double2 *>(A.partial + (size_t)A.tile_base[img] * A.items_per_tile * N * kNO);
-    const size_t istride = (size_t)N * 5;  // double2 per item
-    const double *Gd = reinterpret_cast<const double *>(S.G);
+    const double *Gi = G + (size_t)img * N * kNO;
+    double *sg = s_g[warp];
     OutState st;
     out_init(st, A.c);
     for (int s0 = 0; s0 < N; s0 += kOSteps) {
         const int ns = min(kOSteps, N - s0);
-        for (int j = lane; j < ns; j += 32) {
-            double2 g[5];
-#pragma unroll
-            for (int p = 0; p < 5; ++p) g[p] = make_double2(0.0, 0.0);
-            const double2 *src = P + (size_t)(s0 + j) * 5;
-            for (int i = 0; i < ni; ++i) {
-#pragma unroll
-                for (int p = 0; p < 5; ++p) {
-                    const double2 a = __ldcg(src + i * istride + p);
-                    g[p].x = __dadd_rn(g[p].x, a.x);
-                    g[p].y = __dadd_rn(g[p].y, a.y);
-                }
-            }
-#pragma unroll
-            for (int p = 0; p < 5; ++p) S.G[j * 5 + p] = g[p];
-        }
+        for (int k = lane; k < ns * kNO; k += 32) sg[k] = __ldcs(Gi + (size_t)s0 * kNO + k);
         __syncwarp();
         for (int j = 0; j < ns; ++j) {
             const int s = s0 + j;
             double ff;
-            out_step(st, A.c, Gd[j * kNO + l], s, l, &ff);
+            out_step(st, A.c, sg[j * kNO + l], s, l, &ff);
             if (A.out.out_raster && lane == 0) A.out.out_raster[(size_t)img * N + s] = (uint16_t)st.prev;
             if (lane < kNO) {
                 if (A.out.ff) A.out.ff[((size_t)img * N + s) * kNO + lane] = ff;
@@ -638,7 +724,5 @@ __global__ void __launch_bounds__(kOutWarps * 32) k_output(const BatchArgs A) {
     }
     if (lane < kNO) A.out.counts[(size_t)img * kNO + lane] = st.cnt;
 }
-
-constexpr size_t kOutSmemBytes = sizeof(OutSmem) * kOutWarps;
 
 }  // namespace snn

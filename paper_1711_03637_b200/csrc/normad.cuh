@@ -8,7 +8,7 @@
 // in parallel, and a short weight-dependent part that must run image after
 // image (W_{i+1} = W_i + r * dW_i):
 //
-//   K1 k_hidden<RASTER>   (parallel)  hidden spike raster per image
+//   K1 k_hidden           (parallel)  hidden spike raster per image
 //   K2 k_compact          (parallel)  active-neuron list, per-neuron spike
 //                                     lists, per-step spike lists (CSR), and
 //                                     the d_hat norm of every step
@@ -31,7 +31,7 @@ constexpr int kCThreads = kMaxTiles * 32;  // 704: one thread per (tile, lane) s
 constexpr int kTThreads = 512;             // sequential NormAD CTA (128 regs/thread)
 
 struct TrainWS {
-    uint8_t *raster;    // sum(n_tiles) x N x 64 bytes (raster_at layout)
+    uint8_t *raster;    // sum(n_tiles) x nchunks x 512 bytes (raster_tc layout)
     uint16_t *tile_pos; // [n][22][32]
     int32_t *n_tiles;   // [n]
     int32_t *tile_base; // [n+1]
@@ -101,9 +101,13 @@ __global__ void __launch_bounds__(kCThreads) k_compact(const TrainArgs T) {
     int pos = 0xFFFF;
     if (tile < ntiles) pos = W.tile_pos[((size_t)img * kMaxTiles + tile) * kTile + lane];
     const bool valid = pos != 0xFFFF;
-    const size_t rstride = (size_t)ntiles * 2 * kTile;  // raster step stride of this image
-    const uint8_t *R = W.raster + (tile < ntiles ? raster_at(W.tile_base[img], N, ntiles, 0, tile) : 0) + lane;
-    auto mask12 = [&](int s) { return (unsigned)R[(size_t)s * rstride] | ((unsigned)R[(size_t)s * rstride + kTile] << kHalf); };
+    const size_t rstride = (size_t)ntiles * kRastTC;  // raster chunk stride of this image
+    const uint8_t *R =
+        W.raster + (tile < ntiles ? raster_tc(W.tile_base[img], n_chunks(N), ntiles, 0, tile) : 0) + lane * kChunk;
+    auto mask12 = [&](int s) {
+        const uint8_t *p = R + (size_t)(s / kChunk) * rstride + (s % kChunk);
+        return (unsigned)p[0] | ((unsigned)p[kRastTC / 2] << kHalf);
+    };
 
     // pass 1: which of my 12 neurons ever fire, and how often
     unsigned ever = 0;

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 
 #include "normad.cuh"
 
@@ -38,6 +39,8 @@ int validate(const snn_consts_t *c) {
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
+constexpr int kMaxSub = 64;  // sub-batches of one pipelined snn_infer call
+
 // The specialised kernel is exact for any bank whose taps EQUAL the default
 // ones (+0.0 and -0.0 zero taps are both skipped, see def_current).
 bool is_default_bank(const snn_consts_t &c) {
@@ -51,11 +54,15 @@ bool is_default_bank(const snn_consts_t &c) {
 // (see lif_update); any other sign pattern takes the FP64 compares.
 bool signed_lif(const snn_consts_t &c) { return c.lif_hid.el < 0.0 && c.lif_hid.vt > 0.0; }
 
-// ---- inference workspace: tile_pos | n_tiles | tile_base | partials (upper bound)
+// upper bound of the compact raster of n images (every image at 22 tiles)
+size_t raster_bytes(const snn_consts_t *c, int64_t n) { return (size_t)n * kMaxTiles * n_chunks(c->n_steps) * kRastTC; }
+
+// ---- inference workspace: tile_pos | n_tiles | tile_base | raster (upper bound)
 struct InferWS {
     uint16_t *tile_pos;
     int32_t *n_tiles, *tile_base;
-    double *partial;
+    uint8_t *raster;
+    double *g;  // [n][N][10] G rows (k_gsum -> k_output)
 };
 
 size_t infer_ws_layout(const snn_consts_t *c, int64_t n, char *base, InferWS *w) {
@@ -68,8 +75,10 @@ size_t infer_ws_layout(const snn_consts_t *c, int64_t n, char *base, InferWS *w)
     InferWS x;
     x.tile_pos = (uint16_t *)take((size_t)n * kMaxTiles * kTile * 2);
     x.n_tiles = (int32_t *)take((size_t)n * 4);
-    x.tile_base = (int32_t *)take((size_t)(n + 1) * 4);
-    x.partial = (double *)take((size_t)n * kMaxTiles * (is_default_bank(*c) ? 1 : 2) * c->n_steps * kNO * 8);
+    x.tile_base = (int32_t *)take((size_t)(n + 1 + kMaxSub) * 4);
+    x.raster = (uint8_t *)take(raster_bytes(c, n));
+    x.g = (double *)take((size_t)n * c->n_steps * kNO * 8);
+
     if (w) *w = x;
     return off;
 }
@@ -86,7 +95,7 @@ int64_t train_evcap(const snn_consts_t *c) {
 
 size_t train_ws_per_image(const snn_consts_t *c) {
     const size_t N = c->n_steps, cap = train_evcap(c);
-    return kMaxTiles * N * kTile * 2 + kMaxTiles * kTile * 2 + 4 + 4 + 4 + kNH * 2 + (kNH + 1) * 4 + cap * 2 +
+    return raster_bytes(c, 1) + kMaxTiles * kTile * 2 + 4 + 4 + 4 + kNH * 2 + (kNH + 1) * 4 + cap * 2 +
            (N + 1) * 4 + cap * 2 + N * 8 + kMaxTiles * N * 8;
 }
 
@@ -106,7 +115,7 @@ size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base) 
         return p;
     };
     TrainWS w;
-    w.raster = (uint8_t *)take(n * kMaxTiles * N * kTile * 2);
+    w.raster = (uint8_t *)take(raster_bytes(c, (int64_t)n));
     w.tile_pos = (uint16_t *)take(n * kMaxTiles * kTile * 2);
     w.n_tiles = (int32_t *)take(n * 4);
     w.tile_base = (int32_t *)take((n + 1) * 4);
@@ -136,16 +145,21 @@ int sm_count() {
     return sms;
 }
 
-// prep -> tile scan -> hidden (persistent) [-> output]; raster etc. in A
-template <bool TRACE, bool DEF, bool RASTER, bool GSUM, bool SGN>
-int launch_batch(const BatchArgs &A, bool with_output, cudaStream_t st) {
+// k_hidden CTAs per SM (0 = occupancy limit); snn_set_pipeline
+int g_hid_ctas = 0;
+int64_t g_pipe_images = 0;
+
+// prep -> tile scan -> hidden (persistent): the hidden raster of A's images
+template <bool TRACE, bool DEF, bool SGN>
+int launch_hidden(const BatchArgs &A, cudaStream_t st) {
     static int hid_blocks = 0;
     if (!hid_blocks) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hid_blocks, k_hidden<TRACE, DEF, RASTER, GSUM, SGN>,
-                                                          kThreads, 0) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hid_blocks, k_hidden<TRACE, DEF, SGN>, kThreads, 0) !=
+                cudaSuccess ||
             hid_blocks <= 0)
             hid_blocks = 4;
     }
+    const int per_sm = g_hid_ctas > 0 ? std::min(g_hid_ctas, hid_blocks) : hid_blocks;
     int rc;
     const unsigned n = (unsigned)A.n_images;
     k_prep<<<n, kThreads, 0, st>>>(A);
@@ -153,23 +167,61 @@ int launch_batch(const BatchArgs &A, bool with_output, cudaStream_t st) {
     k_tile_scan<<<1, 1024, 0, st>>>(A);
     if ((rc = cuda_check("k_tile_scan"))) return rc;
     const int64_t max_groups = (2 * A.n_images * kMaxTiles + kWPC - 1) / kWPC;
-    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)hid_blocks * sm_count(), max_groups);
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)per_sm * sm_count(), max_groups);
     if (g_ev_before) cudaEventRecord(g_ev_before, st);
-    k_hidden<TRACE, DEF, RASTER, GSUM, SGN><<<grid, kThreads, 0, st>>>(A);
+    k_hidden<TRACE, DEF, SGN><<<grid, kThreads, 0, st>>>(A);
     if ((rc = cuda_check("k_hidden"))) return rc;
     if (g_ev_after) cudaEventRecord(g_ev_after, st);
-    if (with_output) {
-        k_output<<<(n + kOutWarps - 1) / kOutWarps, kOutWarps * 32, kOutSmemBytes, st>>>(A);
-        if ((rc = cuda_check("k_output"))) return rc;
-    }
     return SNN_OK;
 }
 
+// G rows, then the output layer
+int launch_contract(const BatchArgs &A, double *g, cudaStream_t st) {
+    int rc;
+    const int64_t n = A.n_images;
+    const int64_t tasks = n * n_chunks(A.c.n_steps);
+    k_gsum<<<(unsigned)((tasks + kGWarps - 1) / kGWarps), kGWarps * 32, 0, st>>>(A, g);
+    if ((rc = cuda_check("k_gsum"))) return rc;
+    k_output<<<(unsigned)((n + kOutWarps2 - 1) / kOutWarps2), kOutWarps2 * 32, 0, st>>>(A, g);
+    return cuda_check("k_output");
+}
+
+template <bool TRACE, bool DEF, bool SGN>
+int launch_batch(const BatchArgs &A, double *g, cudaStream_t st) {
+    int rc = launch_hidden<TRACE, DEF, SGN>(A, st);
+    if (rc || !g) return rc;
+    return launch_contract(A, g, st);
+}
+
+template <bool DEF>
+int launch_hidden_fast(const BatchArgs &A, cudaStream_t st) {
+    return signed_lif(A.c) ? launch_hidden<false, DEF, true>(A, st) : launch_hidden<false, DEF, false>(A, st);
+}
+
 // Picks the k_hidden instantiation: TRACE variants always use FP64 compares.
-template <bool DEF, bool RASTER, bool GSUM>
-int launch_fast(const BatchArgs &A, bool with_output, cudaStream_t st) {
-    return signed_lif(A.c) ? launch_batch<false, DEF, RASTER, GSUM, true>(A, with_output, st)
-                           : launch_batch<false, DEF, RASTER, GSUM, false>(A, with_output, st);
+template <bool DEF>
+int launch_fast(const BatchArgs &A, double *g, cudaStream_t st) {
+    return signed_lif(A.c) ? launch_batch<false, DEF, true>(A, g, st) : launch_batch<false, DEF, false>(A, g, st);
+}
+
+// Per-device auxiliary stream + events of the pipelined inference path.
+struct Pipe {
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev[kMaxSub + 1] = {};
+};
+std::mutex g_pipe_mu;
+Pipe g_pipes[64];
+
+Pipe *pipe_for_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    Pipe &p = g_pipes[dev];
+    if (!p.aux) {
+        if (cudaStreamCreateWithFlags(&p.aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        for (auto &e : p.ev)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    }
+    return &p;
 }
 
 // Shared-memory caps of k_normad: as many active neurons / events as fit in
@@ -236,20 +288,49 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
     A.tile_pos = out->tile_pos ? out->tile_pos : w.tile_pos;
     A.n_tiles = out->n_tiles ? out->n_tiles : w.n_tiles;
     A.tile_base = out->tile_base ? out->tile_base : w.tile_base;
-    A.raster = out->raster;
-    A.partial = w.partial;
+    A.raster = out->raster ? out->raster : w.raster;
+
     A.out = *out;
     const bool def = is_default_bank(*c);
     A.items_per_tile = def ? 1 : 2;
-    const bool raster = out->raster != nullptr;
-    if (out->v_hid) {
-        if (raster) return def ? launch_batch<true, true, true, true, false>(A, true, s)
-                               : launch_batch<true, false, true, true, false>(A, true, s);
-        return def ? launch_batch<true, true, false, true, false>(A, true, s)
-                   : launch_batch<true, false, false, true, false>(A, true, s);
+    if (out->v_hid) return def ? launch_batch<true, true, false>(A, w.g, s) : launch_batch<true, false, false>(A, w.g, s);
+    // Pipelined: sub-batches of g_pipe_images; the hidden layer of sub-batch
+    // b+1 (main stream) runs while the contraction + output layer of sub-batch
+    // b run on an auxiliary stream, and each sub-batch's raster is still in L2
+    // when it is read.  Only when no caller-visible raster is requested (that
+    // one is indexed by a single tile_base).
+    const bool caller_raster = out->raster || out->tile_pos || out->n_tiles || out->tile_base;
+    Pipe *pp = (g_pipe_images > 0 && !caller_raster && n > g_pipe_images) ? pipe_for_device() : nullptr;
+    if (!pp) return def ? launch_fast<true>(A, w.g, s) : launch_fast<false>(A, w.g, s);
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    const int64_t per = std::max<int64_t>(g_pipe_images, (n + kMaxSub - 1) / kMaxSub);
+    const int N = c->n_steps, nch = n_chunks(N);
+    int b = 0;
+    for (int64_t i0 = 0; i0 < n; i0 += per, ++b) {
+        BatchArgs B = A;
+        B.images = d_images + i0 * SNN_N_PIXELS;
+        B.n_images = std::min(per, n - i0);
+        B.tile_pos = w.tile_pos + i0 * kMaxTiles * kTile;
+        B.n_tiles = w.n_tiles + i0;
+        B.tile_base = w.tile_base + i0 + b;
+        B.raster = w.raster + (size_t)i0 * kMaxTiles * nch * kRastTC;
+        B.out.counts = out->counts + i0 * kNO;
+        if (out->out_raster) B.out.out_raster = out->out_raster + i0 * N;
+        if (out->ff) B.out.ff = out->ff + i0 * N * kNO;
+        if (out->v_out) B.out.v_out = out->v_out + i0 * N * kNO;
+        if ((rc = def ? launch_hidden_fast<true>(B, s) : launch_hidden_fast<false>(B, s))) return rc;
+        cudaEventRecord(pp->ev[b], s);
+        cudaStreamWaitEvent(pp->aux, pp->ev[b], 0);
+        if ((rc = launch_contract(B, w.g + (size_t)i0 * N * kNO, pp->aux))) return rc;
     }
-    if (raster) return def ? launch_fast<true, true, true>(A, true, s) : launch_fast<false, true, true>(A, true, s);
-    return def ? launch_fast<true, false, true>(A, true, s) : launch_fast<false, false, true>(A, true, s);
+    cudaEventRecord(pp->ev[kMaxSub], pp->aux);
+    cudaStreamWaitEvent(s, pp->ev[kMaxSub], 0);
+    return cuda_check("snn_infer pipeline");
+}
+
+extern "C" void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_per_sm) {
+    g_pipe_images = images_per_subbatch;
+    g_hid_ctas = hidden_ctas_per_sm;
 }
 
 extern "C" size_t snn_train_workspace(const snn_consts_t *c, int64_t n) {
@@ -297,8 +378,7 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
         A.n_tiles = T.ws.n_tiles;
         A.tile_base = T.ws.tile_base;
         A.items_per_tile = is_default_bank(*c) ? 1 : 2;
-        if ((rc = is_default_bank(*c) ? launch_fast<true, true, false>(A, false, s)
-                                      : launch_fast<false, true, false>(A, false, s)))
+        if ((rc = is_default_bank(*c) ? launch_fast<true>(A, nullptr, s) : launch_fast<false>(A, nullptr, s)))
             return rc;
         T.n = cn;
         T.first = i0;

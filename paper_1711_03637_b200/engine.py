@@ -125,8 +125,7 @@ class Engine:
         with torch.cuda.stream(self.stream):
             out = {"counts": torch.empty((n, N_OUTPUTS), dtype=torch.int32, device=dev)}
             if raster:  # compact layout, see include/snn_b200.h
-                out["raster"] = torch.empty((n * _native.MAX_TILES * N * 2 * _native.TILE,), dtype=torch.uint8,
-                                            device=dev)
+                out["raster"] = torch.empty((_native.raster_bytes(n, N),), dtype=torch.uint8, device=dev)
                 out["tile_pos"] = torch.empty((n, _native.MAX_TILES, _native.TILE), dtype=torch.int16, device=dev)
                 out["n_tiles"] = torch.empty((n,), dtype=torch.int32, device=dev)
                 out["tile_base"] = torch.empty((n + 1,), dtype=torch.int32, device=dev)

@@ -1,6 +1,9 @@
 """Distill ncu captures and launch lists (gpurun_out/) into profiles/<tag>_*.
 
-  python scripts/summarize_profiles.py r01
+  python scripts/summarize_profiles.py r01 [RUN]
+
+RUN selects one gpu_iter.sh run (gpurun_out/{prof,launches,bench}_RUN.*);
+without it every .ncu-rep in gpurun_out/ is summarised.
 
 Writes profiles/<tag>_ncu_summary.md (key metrics + top stall reasons + the
 hottest source lines per kernel), profiles/<tag>_launches.csv (per-launch
@@ -82,13 +85,20 @@ def summarize(rep, fh):
 
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    run = sys.argv[2] if len(sys.argv) > 2 else None
     os.makedirs(PROF, exist_ok=True)
+    reps = [f"prof_{run}.ncu-rep"] if run else sorted(f for f in os.listdir(OUT) if f.endswith(".ncu-rep"))
     with open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w") as fh:
         fh.write(f"# ncu summary ({tag})\n\nFrom `ncu --set full --clock-control none --import-source on` "
                  "captures (cold-cache, serialised replays: compare shares, not absolutes).\n")
-        for rep in sorted(f for f in os.listdir(OUT) if f.endswith(".ncu-rep")):
+        for rep in reps:
             fh.write(f"\n## {rep}\n")
             summarize(os.path.join(OUT, rep), fh)
+    if run:
+        for src, dst in ((f"launches_{run}.csv", "launches.csv"), (f"bench_{run}.json", "bench.json")):
+            if os.path.exists(os.path.join(OUT, src)):
+                import shutil
+                shutil.copy(os.path.join(OUT, src), os.path.join(OUT, dst))
     for f in ("launches.csv", "launches_train.csv"):
         src = os.path.join(OUT, f)
         if os.path.exists(src):

@@ -310,3 +310,46 @@ def test_custom_filter_bank_generic_kernel(sd, cfg, workloads, oracle):
         for nidx, steps in enumerate(rec.hidden_spikes):
             hm[steps, nidx] = True
         assert np.array_equal(hm, recs[k]["hidden"])
+
+
+# ------------------------------------------------------------------ config 5: 60k NormAD pass + 10k eval
+def test_c5_full_pass_vs_reference(sd, cfg, bank):
+    """SURVEY 8(d) config 5 end to end: one online NormAD pass over the 60,000
+    images of synthetic_dataset(6000, seed=4000) from zero weights, then the
+    10,000-image eval -- against the reference's own run of the same pass
+    (oracle/gen_c5.py -> tests/golden/c5_reference.npz)."""
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    d5 = np.load(os.path.join(root, "data", "c5_workload.npz"))
+    g = np.load(os.path.join(root, "tests", "golden", "c5_reference.npz"))
+    from paper_1711_03637_b200.engine import get_engine, make_consts
+    order = d5["order"]
+    tr, lab = d5["train_images"][order], d5["train_labels"][order]
+    eng = get_engine()
+    learn = sd.LearnConfig()
+    c = make_consts(cfg, bank, learn)
+    d_tr = torch.from_numpy(tr.reshape(len(tr), -1).copy()).to(eng.device)
+    d_lab = torch.from_numpy(lab.astype(np.uint8)).to(eng.device)
+    d_w = torch.zeros((8112, 10), dtype=torch.float64, device=eng.device)
+    snaps = {}
+    done = 0
+    for stop in (1000, 10000, 60000):
+        counts, status = eng.train(c, d_tr[done:stop], d_lab[done:stop], d_w)
+        eng.stream.synchronize()
+        assert status.cpu().tolist()[0] == 0
+        snaps[stop] = (d_w.cpu().numpy(), counts.cpu().numpy())
+        done = stop
+    for stop, (w, _) in snaps.items():
+        ref = g[f"w_after_{stop}"]
+        rel = float(np.abs(w - ref).max() / np.abs(ref).max())
+        print(f"c5 W after {stop}: max rel err vs reference {rel:.3e}")
+        assert rel <= 1e-4, (stop, rel)
+    ctr = np.concatenate([snaps[k][1] for k in (1000, 10000, 60000)])
+    same = float((ctr == g["train_counts"]).all(axis=1).mean())
+    print(f"c5 per-image training counts identical: {same:.6f}")
+    assert same >= 0.999
+    w = snaps[60000][0]
+    ev = sd.batch_counts(d5["eval_images"][:500], w, bank, cfg)
+    same_ev = float((ev == g["eval_counts_500"]).all(axis=1).mean())
+    assert same_ev >= 0.999
+    assert np.mean(np.argmax(ev, 1) == np.argmax(g["eval_counts_500"], 1)) >= 0.999

@@ -97,15 +97,17 @@ def test_decode_hidden_roundtrip():
     want = np.zeros((N, 8112), dtype=bool)
     active = np.sort(rng.choice(676, size=70, replace=False))
     nt = 3
-    raster = np.zeros((tb + nt) * N * 64, dtype=np.uint8)
-    blk = raster[tb * N * 64:].reshape(N, nt, 2, 32)
+    nch = -(-N // 8)
+    raster = np.zeros((tb + nt) * nch * 512, dtype=np.uint8)
+    blk = raster[tb * nch * 512:].reshape(nch, nt, 2, 32, 8)
     tpos = np.full((22, 32), -1, dtype=np.int16)
     for slot, p in enumerate(active):
         t, lane = divmod(slot, 32)
         tpos[t, lane] = p
         m = rng.integers(0, 4096, size=N) & rng.integers(0, 4096, size=N)
-        blk[:, t, 0, lane] = m & 0x3F
-        blk[:, t, 1, lane] = m >> 6
+        for s_ in range(N):
+            blk[s_ // 8, t, 0, lane, s_ % 8] = m[s_] & 0x3F
+            blk[s_ // 8, t, 1, lane, s_ % 8] = m[s_] >> 6
         for f in range(12):
             want[:, p * 12 + f] = (m >> f) & 1
     got = decode_hidden(raster, tb, tpos, nt, N)
