@@ -128,6 +128,16 @@ void snn_profile_events(void *before, void *after);
  * no gain on one B200 -- the persistent k_hidden leaves no room to overlap). */
 void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_per_sm);
 
+/* snn_train runs its sequential NormAD chain on a cluster of 8 CTAs that
+ * keeps W in distributed shared memory (default, enable = 1) when N <= ~600,
+ * else on one CTA; enable = 0 forces the one-CTA kernel (same results). */
+void snn_set_normad_cluster(int enable);
+
+/* Profiling hook: when d_clk (device, int64 [64][16]) is set, the cluster
+ * NormAD kernel records clock64() at its phase boundaries for the first 64
+ * images of each snn_train call (NULL disables). */
+void snn_normad_phase_clocks(long long *d_clk);
+
 /* Bytes of device workspace snn_train needs for n images. */
 size_t snn_train_workspace(const snn_consts_t *c, int64_t n_images);
 

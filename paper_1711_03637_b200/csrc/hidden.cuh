@@ -437,21 +437,31 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
 // ---------------------------------------------------------------------------
 // Output layer state and one step of it (network.py:308-314), lanes 0..9 of
 // one warp = the 10 output neurons (lanes 10..31 shadow lane 9, harmlessly).
-// Every lane keeps all ten lateral-inhibition traces and advances them from
-// the previous step's spike ballot, so the inhibition sum needs no shuffles
-// on the serial path (same operations as the reference, so bit-identical).
+// Every lane keeps all ten lateral-inhibition traces, so the inhibition sum
+// needs no shuffles.  The serial chain is cut short by speculation: the
+// traces enter step s as a*e^{-dt/tau} (their values before this step's
+// spike input), and the no-spike outcome -- S0 = pairwise sum of the ten
+// c = a - b and this lane's own c0 -- is computed one step ahead, off the
+// chain.  After a step without output spikes (most steps) the next step
+// only needs S0; otherwise the bumps are added and the sum is redone.  Every
+// value is the reference's own operation sequence (a*lam + 0 == a*lam
+// exactly for a >= 0), so results are bit-identical either way.
 struct OutState {
-    double Af, Bf;           // event-driven feed-forward recursions (slow, fast)
-    double ao[kNO], bo[kNO]; // lateral-inhibition kernels of all output neurons
+    double Af, Bf;             // event-driven feed-forward recursions (slow, fast)
+    double al[kNO], bl[kNO];   // inhibition traces times their decay (before this step's bumps)
+    double al_o, bl_o;         // the same for this lane's own neuron
+    double S0, c0;             // pairwise sum and own trace if no output spiked last step
     double v;
     int live_from, cnt;
-    unsigned prev;           // output spikes of the previous step (10-bit)
+    unsigned prev;             // output spikes of the previous step (10-bit)
 };
 
 __device__ __forceinline__ void out_init(OutState &st, const snn_consts_t &c) {
     st.Af = st.Bf = 0.0;
 #pragma unroll
-    for (int k = 0; k < kNO; ++k) st.ao[k] = st.bo[k] = 0.0;
+    for (int k = 0; k < kNO; ++k) st.al[k] = st.bl[k] = 0.0;
+    st.al_o = st.bl_o = 0.0;
+    st.S0 = st.c0 = 0.0;  // pairwise10 of ten +0 is +0
     st.v = c.lif_out.el;
     st.live_from = 0;
     st.cnt = 0;
@@ -465,24 +475,59 @@ __device__ __forceinline__ bool out_step(OutState &st, const snn_consts_t &c, do
     st.Af = __dadd_rn(__dmul_rn(st.Af, c.decay_slow), G);
     st.Bf = __dadd_rn(__dmul_rn(st.Bf, c.decay_fast), G);
     const double ff = __dsub_rn(st.Af, st.Bf);
-    double cc[kNO], co = 0.0;
+    // inhibition traces after this step's bumps (the previous step's output spikes)
+    double a[kNO], b[kNO], ao, bo, S, co;
+    if (st.prev == 0u) {  // warp-uniform
 #pragma unroll
-    for (int k = 0; k < kNO; ++k) {  // inhibition sees last step's spikes
-        const double bump = ((st.prev >> k) & 1u) ? 1.0 : 0.0;
-        st.ao[k] = __dadd_rn(__dmul_rn(st.ao[k], c.decay_slow), bump);
-        st.bo[k] = __dadd_rn(__dmul_rn(st.bo[k], c.decay_fast), bump);
-        cc[k] = __dsub_rn(st.ao[k], st.bo[k]);
-        co = k == l ? cc[k] : co;
+        for (int k = 0; k < kNO; ++k) {
+            a[k] = st.al[k];
+            b[k] = st.bl[k];
+        }
+        ao = st.al_o;
+        bo = st.bl_o;
+        S = st.S0;
+        co = st.c0;
+    } else {
+        double cc[kNO];
+#pragma unroll
+        for (int k = 0; k < kNO; ++k) {
+            const double bump = ((st.prev >> k) & 1u) ? 1.0 : 0.0;
+            a[k] = __dadd_rn(st.al[k], bump);
+            b[k] = __dadd_rn(st.bl[k], bump);
+            cc[k] = __dsub_rn(a[k], b[k]);
+        }
+        const double bo_ = ((st.prev >> l) & 1u) ? 1.0 : 0.0;
+        ao = __dadd_rn(st.al_o, bo_);
+        bo = __dadd_rn(st.bl_o, bo_);
+        S = pairwise10(cc);
+        co = __dsub_rn(ao, bo);
     }
-    const double S = pairwise10(cc);
     const double drive = __dadd_rn(ff, __dmul_rn(c.inhibition, __dsub_rn(S, co)));
-    const double cand = lif_candidate(st.v, drive, c.lif_out);
+    // LIF (neurons.py:113-126); a refractory neuron holds v == E_L
+    const snn_lif_t &p = c.lif_out;
+    double t = __dsub_rn(st.v, p.el);
+    t = __dmul_rn(p.g, t);
+    t = __dsub_rn(drive, t);
+    t = __dmul_rn(p.beta, t);
+    const double vn = __dadd_rn(st.v, t);
     const bool live = s >= st.live_from;
-    const bool fired = live && cand >= c.lif_out.vt;
-    if (live) st.v = fired ? c.lif_out.el : cand;
-    if (fired) st.live_from = next_live_step(s, c.lif_out.refr);
+    const bool fired = live && vn >= p.vt;
+    st.v = (!live || fired || vn < p.el) ? p.el : vn;
+    if (fired) st.live_from = next_live_step(s, p.refr);
     st.prev = __ballot_sync(kFull, fired) & 0x3FFu;
     st.cnt += fired ? 1 : 0;
+    // the next step's decayed traces and its no-spike outcome, off the chain
+    double cc0[kNO];
+#pragma unroll
+    for (int k = 0; k < kNO; ++k) {
+        st.al[k] = __dmul_rn(a[k], c.decay_slow);
+        st.bl[k] = __dmul_rn(b[k], c.decay_fast);
+        cc0[k] = __dsub_rn(st.al[k], st.bl[k]);
+    }
+    st.al_o = __dmul_rn(ao, c.decay_slow);
+    st.bl_o = __dmul_rn(bo, c.decay_fast);
+    st.S0 = pairwise10(cc0);
+    st.c0 = __dsub_rn(st.al_o, st.bl_o);
     *ff_out = ff;
     return fired;
 }

@@ -6,7 +6,7 @@
 #include <cstring>
 #include <mutex>
 
-#include "normad.cuh"
+#include "normad_cl.cuh"
 
 using namespace snn;
 
@@ -96,7 +96,8 @@ int64_t train_evcap(const snn_consts_t *c) {
 size_t train_ws_per_image(const snn_consts_t *c) {
     const size_t N = c->n_steps, cap = train_evcap(c);
     return raster_bytes(c, 1) + kMaxTiles * kTile * 2 + 4 + 4 + 4 + kNH * 2 + (kNH + 1) * 4 + cap * 2 +
-           (N + 1) * 4 + cap * 2 + N * 8 + kMaxTiles * N * 8;
+           (N + 1) * 4 + cap * 2 + N * 8 + kMaxTiles * N * 8 + 2 * (kCl + 1) * 4 + kCl * (N + 1) * 4 + cap * 2 + N * 8 +
+           (size_t)kCl * kClRows * kNO * 8 / 64;
 }
 
 int64_t train_chunk(const snn_consts_t *c, int64_t n) {
@@ -106,7 +107,7 @@ int64_t train_chunk(const snn_consts_t *c, int64_t n) {
     return std::min<int64_t>(ch, std::max<int64_t>(n, 1));
 }
 
-size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base) {
+size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base, ShardWS *sh = nullptr) {
     const size_t N = c->n_steps, cap = train_evcap(c), n = chunk;
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -128,7 +129,16 @@ size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base) 
     w.norm = (double *)take(n * N * 8);
     w.wp = (double *)take(n * kMaxTiles * N * 8);
     w.evcap = (int64_t)cap;
+    ShardWS x;
+    x.clk = nullptr;
+    x.act = (int32_t *)take(n * (kCl + 1) * 4);
+    x.soff = (int32_t *)take(n * kCl * (N + 1) * 4);
+    x.ebase = (int32_t *)take(n * (kCl + 1) * 4);
+    x.sid = (uint16_t *)take(n * cap * 2);
+    x.q = (double *)take(n * N * 8);
+    x.undo = (double *)take((size_t)kCl * kClRows * kNO * 8);
     if (out) *out = w;
+    if (sh) *sh = x;
     return off;
 }
 
@@ -147,6 +157,8 @@ int sm_count() {
 
 // k_hidden CTAs per SM (0 = occupancy limit); snn_set_pipeline
 int g_hid_ctas = 0;
+int g_normad_cluster = 1;  // snn_set_normad_cluster
+long long *g_phase_clk = nullptr;  // snn_normad_phase_clocks
 int64_t g_pipe_images = 0;
 
 // prep -> tile scan -> hidden (persistent): the hidden raster of A's images
@@ -328,6 +340,10 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
     return cuda_check("snn_infer pipeline");
 }
 
+extern "C" void snn_set_normad_cluster(int enable) { g_normad_cluster = enable; }
+
+extern "C" void snn_normad_phase_clocks(long long *d_clk) { g_phase_clk = d_clk; }
+
 extern "C" void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_per_sm) {
     g_pipe_images = images_per_subbatch;
     g_hid_ctas = hidden_ctas_per_sm;
@@ -351,16 +367,25 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     if (!d_images || !d_labels || !d_w || !d_ctab || !d_counts) return set_error(SNN_EINVAL, "NULL pointer");
     if (((uintptr_t)d_images & 15) != 0) return set_error(SNN_EINVAL, "images must be 16-byte aligned");
     if (c->n_steps > 65535) return set_error(SNN_EINVAL, "training supports n_steps <= 65535");
+    // the W-resident cluster kernel when its shared memory fits, else the one-CTA kernel
+    const size_t cl_smem = normad_cl_smem_bytes(c->n_steps);
+    const bool use_cl = g_normad_cluster && cl_smem <= 227 * 1024;
     const NormadCaps caps = normad_caps(c);
     const size_t smem = normad_smem_bytes(c->n_steps, caps);
-    if (smem > 220 * 1024) return set_error(SNN_EINVAL, "n_steps too large for the sequential NormAD CTA");
+    if (!use_cl && smem > 220 * 1024) return set_error(SNN_EINVAL, "n_steps too large for the sequential NormAD CTA");
     const int64_t chunk = train_chunk(c, n);
     TrainArgs T;
     memset(&T, 0, sizeof(T));
-    const size_t need = train_ws(c, chunk, &T.ws, (char *)d_ws);
+    ShardWS SW;
+    const size_t need = train_ws(c, chunk, &T.ws, (char *)d_ws, &SW);
+    SW.clk = g_phase_clk;
     if (!d_ws || ws_bytes < need) return set_error(SNN_ENOMEM, "workspace too small");
-    if (cudaFuncSetAttribute(k_normad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (use_cl) {
+        if (cudaFuncSetAttribute(k_normad_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem) != cudaSuccess)
+            return cuda_check("cudaFuncSetAttribute(k_normad_cl)");
+    } else if (cudaFuncSetAttribute(k_normad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         return cuda_check("cudaFuncSetAttribute(k_normad)");
+    }
     T.c = *c;
     T.w = d_w;
     T.status = d_status;
@@ -386,8 +411,15 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
         T.counts = d_counts + i0 * kNO;
         k_compact<<<(unsigned)cn, kCThreads, 0, s>>>(T);
         if ((rc = cuda_check("k_compact"))) return rc;
-        k_normad<<<1, kTThreads, smem, s>>>(T, caps);
-        if ((rc = cuda_check("k_normad"))) return rc;
+        if (use_cl) {
+            k_shard<<<(unsigned)cn, 256, k_shard_smem(c->n_steps), s>>>(T, SW);
+            if ((rc = cuda_check("k_shard"))) return rc;
+            k_normad_cl<<<kCl, kClThreads, cl_smem, s>>>(T, SW);
+            if ((rc = cuda_check("k_normad_cl"))) return rc;
+        } else {
+            k_normad<<<1, kTThreads, smem, s>>>(T, caps);
+            if ((rc = cuda_check("k_normad"))) return rc;
+        }
     }
     return SNN_OK;
 }
