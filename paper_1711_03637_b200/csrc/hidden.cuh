@@ -502,6 +502,19 @@ __device__ __forceinline__ bool out_step(OutState &st, const snn_consts_t &c, do
         S = pairwise10(cc);
         co = __dsub_rn(ao, bo);
     }
+    // the next step's decayed traces and its no-spike outcome: independent of
+    // this step's chain, issued before it so the two interleave
+    double cc0[kNO];
+#pragma unroll
+    for (int k = 0; k < kNO; ++k) {
+        st.al[k] = __dmul_rn(a[k], c.decay_slow);
+        st.bl[k] = __dmul_rn(b[k], c.decay_fast);
+        cc0[k] = __dsub_rn(st.al[k], st.bl[k]);
+    }
+    st.al_o = __dmul_rn(ao, c.decay_slow);
+    st.bl_o = __dmul_rn(bo, c.decay_fast);
+    st.S0 = pairwise10(cc0);
+    st.c0 = __dsub_rn(st.al_o, st.bl_o);
     const double drive = __dadd_rn(ff, __dmul_rn(c.inhibition, __dsub_rn(S, co)));
     // LIF (neurons.py:113-126); a refractory neuron holds v == E_L
     const snn_lif_t &p = c.lif_out;
@@ -516,18 +529,6 @@ __device__ __forceinline__ bool out_step(OutState &st, const snn_consts_t &c, do
     if (fired) st.live_from = next_live_step(s, p.refr);
     st.prev = __ballot_sync(kFull, fired) & 0x3FFu;
     st.cnt += fired ? 1 : 0;
-    // the next step's decayed traces and its no-spike outcome, off the chain
-    double cc0[kNO];
-#pragma unroll
-    for (int k = 0; k < kNO; ++k) {
-        st.al[k] = __dmul_rn(a[k], c.decay_slow);
-        st.bl[k] = __dmul_rn(b[k], c.decay_fast);
-        cc0[k] = __dsub_rn(st.al[k], st.bl[k]);
-    }
-    st.al_o = __dmul_rn(ao, c.decay_slow);
-    st.bl_o = __dmul_rn(bo, c.decay_fast);
-    st.S0 = pairwise10(cc0);
-    st.c0 = __dsub_rn(st.al_o, st.bl_o);
     *ff_out = ff;
     return fired;
 }

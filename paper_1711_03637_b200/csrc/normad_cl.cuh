@@ -4,8 +4,9 @@
 // must run image after image: W_{i+1} = W_i + r * dW_i.  k_normad (normad.cuh)
 // runs it on one CTA and re-stages the W rows of every image from global
 // memory.  Here a cluster of kCl CTAs keeps the whole weight matrix resident
-// in distributed shared memory for the whole chunk of images -- CTA r owns
-// rows [r * kClRows, (r + 1) * kClRows) (81 KB each).  Per image i:
+// in distributed shared memory for the whole chunk of images -- CTA r owns the
+// rows of the windows w = r, r + 8, r + 16, ... (81.6 KB each; interleaving
+// the windows balances the spiking neurons over the CTAs).  Per image i:
 //
 //   G partials  every CTA sums, per step, the W rows of its shard's spiking
 //               neurons in ascending id: P_r(s, l)
@@ -39,21 +40,32 @@ namespace snn {
 namespace cg = cooperative_groups;
 
 constexpr int kCl = 8;                          // CTAs per cluster = W shards
-constexpr int kClRows = (kNH + kCl - 1) / kCl;  // 1014 rows per shard
+constexpr int kClWin = (kNPos + kCl - 1) / kCl;  // 85 windows per shard (w % kCl == r)
+constexpr int kClRows = kClWin * kNF;            // 1020 rows per shard
+
+// neuron id <-> (shard, shard-local row)
+__host__ __device__ inline int cl_shard(int id) { return (id / kNF) % kCl; }
+__host__ __device__ inline int cl_row(int id) { return (id / kNF) / kCl * kNF + id % kNF; }
+__host__ __device__ inline int cl_id(int r, int row) { return ((row / kNF) * kCl + r) * kNF + row % kNF; }
+__host__ __device__ inline int cl_rows(int r) { return (kNPos - r + kCl - 1) / kCl * kNF; }
 constexpr int kClThreads = 512;
 constexpr int kClECap = 3072;                   // staged spike events per shard and image
 constexpr int kClACap = 512;                    // staged active neurons per shard and image
 
-// Per-image shard data written by k_shard.  Lists are in ascending neuron id,
-// so every shard's share of the active list and of each step list is one
-// contiguous segment.
+// Per-image shard data written by k_shard (shard-major blocks, each in
+// ascending neuron id).
 struct ShardWS {
     long long *clk;   // optional [64][16] leader phase clocks (snn_normad_phase_clocks)
-    int32_t *act;     // [n][kCl + 1]     first active index of each shard
-    int32_t *soff;    // [n][kCl][N + 1]  per shard: start of each step in its id block
-    int32_t *ebase;   // [n][kCl + 1]     start of each shard's id block in sid
-    uint16_t *sid;    // [n][evcap]       shard-major step lists, shard-local rows
-    double *q;        // [n][N]           dt / |d_hat(s)|, 0 where the gate is closed
+    double *q;        // [n][N]            dt / |d_hat(s)|, 0 where the gate is closed
+    int32_t *soff;    // [n][kCl][N + 1]   per shard: start of each step in its id block
+    int32_t *ebase;   // [n][kCl + 1]      start of each shard's id block in sid
+    uint16_t *sid;    // [n][evcap]        shard-major step lists, shard-local rows
+    int32_t *abase;   // [n][kCl + 1]      start of each shard's neurons in sact
+    uint16_t *sact;   // [n][kNH]          shard-major active neurons, shard-local rows
+    uint16_t *sidx;   // [n][kNH]          ... and their index in the active list
+    int32_t *saoff;   // [n][kNH + kCl]    per shard: start of each neuron's spikes in its block (+ end)
+    int32_t *nbase;   // [n][kCl + 1]      start of each shard's spike block in snsp
+    uint16_t *snsp;   // [n][evcap]        shard-major spike steps of the active neurons
     double *undo;     // [kCl][kClRows][10] old rows of the last committed image
 };
 
@@ -62,10 +74,10 @@ struct ShardWS {
 struct ClBuf {
     const int32_t *soff;   // [N + 1] relative to the id block
     const uint16_t *sid;   // shard-local rows
-    const uint16_t *act;   // global ids of the shard's active neurons
-    const int32_t *aoff;   // [n_act + 1] spike-list offsets (minus abias)
+    const uint16_t *act;   // shard-local rows of the shard's active neurons
+    const int32_t *aoff;   // [n_act + 1] start of each neuron's spikes in nsp
     const uint16_t *nsp;   // spike steps
-    int n_act, abias;
+    int n_act;
 };
 
 __host__ __device__ inline size_t cl_buf_bytes(int N) {
@@ -80,61 +92,119 @@ __host__ __device__ inline size_t normad_cl_smem_bytes(int N) {
            + 2 * ((cl_buf_bytes(N) + 15) & ~(size_t)15);
 }
 
-__host__ __device__ inline size_t k_shard_smem(int N) { return (size_t)N * kCl * 4; }
+// k_shard: grid = images.  dt / |d_hat(s)|, and the image's active neurons,
+// their spike lists and the step lists regrouped shard by shard (stable, so
+// ascending id within every shard), as shard-local rows.
+constexpr int kShThreads = 256;
 
-// k_shard: grid = images.  Shard boundaries, shard-major step lists with
-// shard-local rows, and dt / |d_hat(s)|.
-__global__ void __launch_bounds__(256) k_shard(const TrainArgs T, const ShardWS S) {
+__global__ void __launch_bounds__(kShThreads) k_shard(const TrainArgs T, const ShardWS S) {
     const int64_t i = blockIdx.x;
     const int N = T.c.n_steps;
     const TrainWS &W = T.ws;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kWarps = kShThreads / 32;
     const int n_act = W.n_act[i];
     const uint16_t *act_k = W.act_k + (size_t)i * kNH;
+    const int32_t *aoff = W.act_off + (size_t)i * (kNH + 1);
+    const uint16_t *nsp = W.nsp + (size_t)i * W.evcap;
     const int32_t *soff = W.step_off + (size_t)i * (N + 1);
     const uint16_t *sk = W.step_k + (size_t)i * W.evcap;
-    __shared__ int s_act[kCl + 1];
-    __shared__ int s_base[kCl + 1];
-    extern __shared__ int s_len[];  // [N][kCl] segment lengths, then their offsets
-    if (threadIdx.x <= kCl) {
-        const int r = threadIdx.x;
-        int lo = 0, hi = n_act;  // first active index with id >= r * kClRows
-        const int key = r * kClRows;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if ((int)act_k[mid] < key) lo = mid + 1;
-            else hi = mid;
-        }
-        s_act[r] = r == kCl ? n_act : lo;
-        S.act[i * (kCl + 1) + r] = s_act[r];
-    }
-    const double *nrm = W.norm + (size_t)i * N;
-    for (int s = threadIdx.x; s < N; s += blockDim.x) {
-        const double nv = nrm[s];
+    __shared__ int s_cnt[kCl], s_run[kCl], s_abase[kCl + 1], s_nbase[kCl + 1], s_ebase[kCl + 1];
+    __shared__ int s_wc[kWarps][kCl];
+    extern __shared__ int s_len[];  // [N][kCl] step-list counts, then offsets
+    for (int s = tid; s < N; s += kShThreads) {
+        const double nv = W.norm[(size_t)i * N + s];
         S.q[(size_t)i * N + s] = nv > T.c.norm_eps ? __ddiv_rn(T.c.dt, nv) : 0.0;
     }
-    __syncthreads();
-    // segment [lo, hi) of shard r in step s's list
-    auto seg = [&](int s, int r, int &lo, int &hi) {
-        auto lower = [&](int key) {
-            int a = soff[s], b = soff[s + 1];
-            while (a < b) {
-                const int mid = (a + b) >> 1;
-                if ((int)sk[mid] < key) a = mid + 1;
-                else b = mid;
-            }
-            return a;
-        };
-        lo = lower(s_act[r]);
-        hi = r + 1 < kCl ? lower(s_act[r + 1]) : soff[s + 1];
-    };
-    for (int t = threadIdx.x; t < N * kCl; t += blockDim.x) {
-        int lo, hi;
-        seg(t / kCl, t % kCl, lo, hi);
-        s_len[t] = hi - lo;
+    if (tid < kCl) {
+        s_cnt[tid] = 0;
+        s_run[tid] = 0;
     }
     __syncthreads();
-    if (threadIdx.x < kCl) {  // per-shard prefix over steps
-        const int r = threadIdx.x;
+    // ---- active neurons: counts and spike totals per shard, then a stable partition
+    for (int a = tid; a < n_act; a += kShThreads) atomicAdd(&s_cnt[cl_shard(act_k[a])], 1);
+    __syncthreads();
+    if (tid == 0) {
+        s_abase[0] = 0;
+        for (int r = 0; r < kCl; ++r) s_abase[r + 1] = s_abase[r] + s_cnt[r];
+    }
+    __syncthreads();
+    uint16_t *sact = S.sact + (size_t)i * kNH, *sidx = S.sidx + (size_t)i * kNH;
+    for (int a0 = 0; a0 < n_act; a0 += kShThreads) {
+        const int a = a0 + tid;
+        const int r = a < n_act ? cl_shard(act_k[a]) : -1;
+        int rank = 0;
+#pragma unroll
+        for (int q = 0; q < kCl; ++q) {
+            const unsigned b = __ballot_sync(kFull, r == q);
+            if (r == q) rank = __popc(b & ((1u << lane) - 1u));
+            if (lane == 0) s_wc[warp][q] = __popc(b);
+        }
+        __syncthreads();
+        if (r >= 0) {
+            int pos = s_abase[r] + s_run[r] + rank;
+            for (int w = 0; w < warp; ++w) pos += s_wc[w][r];
+            sact[pos] = (uint16_t)cl_row(act_k[a]);
+            sidx[pos] = (uint16_t)a;
+        }
+        __syncthreads();
+        if (tid < kCl)
+            for (int w = 0; w < kWarps; ++w) s_run[tid] += s_wc[w][tid];
+        __syncthreads();
+    }
+    // per-shard spike-block offsets: warp r walks shard r's neurons in order
+    int32_t *saoff = S.saoff + (size_t)i * (kNH + kCl);
+    if (warp < kCl) {
+        const int r = warp, b0 = s_abase[r], b1 = s_abase[r + 1];
+        int run = 0;
+        for (int k0 = b0; k0 < b1; k0 += 32) {
+            const int k = k0 + lane;
+            const int a = k < b1 ? sidx[k] : 0;
+            const int len = k < b1 ? aoff[a + 1] - aoff[a] : 0;
+            int tot;
+            const int ex = warp_excl_scan_int(len, &tot);
+            if (k < b1) saoff[k + r] = run + ex;
+            run += tot;
+        }
+        if (lane == 0) {
+            saoff[b1 + r] = run;
+            s_cnt[r] = run;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        s_nbase[0] = 0;
+        for (int r = 0; r < kCl; ++r) s_nbase[r + 1] = s_nbase[r] + s_cnt[r];
+        for (int r = 0; r <= kCl; ++r) {
+            S.abase[i * (kCl + 1) + r] = s_abase[r];
+            S.nbase[i * (kCl + 1) + r] = s_nbase[r];
+        }
+    }
+    __syncthreads();
+    uint16_t *snsp = S.snsp + (size_t)i * W.evcap;
+    for (int k = tid; k < n_act; k += kShThreads) {  // shard-major spike blocks
+        int r = 0;
+        while (k >= s_abase[r + 1]) ++r;
+        const int a = sidx[k];
+        uint16_t *dst = snsp + s_nbase[r] + saoff[k + r];
+        for (int e = aoff[a]; e < aoff[a + 1]; ++e) *dst++ = nsp[e];
+    }
+    // ---- step lists: counts per (step, shard), offsets, stable scatter
+    for (int s = tid; s < N; s += kShThreads) {
+        int cnt[kCl];
+#pragma unroll
+        for (int r = 0; r < kCl; ++r) cnt[r] = 0;
+        for (int e = soff[s]; e < soff[s + 1]; ++e) {
+            const int r = cl_shard(act_k[sk[e]]);
+#pragma unroll
+            for (int q = 0; q < kCl; ++q) cnt[q] += q == r;
+        }
+#pragma unroll
+        for (int r = 0; r < kCl; ++r) s_len[s * kCl + r] = cnt[r];
+    }
+    __syncthreads();
+    if (tid < kCl) {  // per-shard prefix over steps
+        const int r = tid;
         int run = 0;
         int32_t *so = S.soff + ((size_t)i * kCl + r) * (N + 1);
         for (int s = 0; s < N; ++s) {
@@ -144,24 +214,32 @@ __global__ void __launch_bounds__(256) k_shard(const TrainArgs T, const ShardWS 
             run += len;
         }
         so[N] = run;
-        s_base[r + 1] = run;
+        s_cnt[r] = run;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        s_base[0] = 0;
-        for (int r = 0; r < kCl; ++r) s_base[r + 1] += s_base[r];
-        for (int r = 0; r <= kCl; ++r) S.ebase[i * (kCl + 1) + r] = s_base[r];
+    if (tid == 0) {
+        s_ebase[0] = 0;
+        for (int r = 0; r < kCl; ++r) s_ebase[r + 1] = s_ebase[r] + s_cnt[r];
+        for (int r = 0; r <= kCl; ++r) S.ebase[i * (kCl + 1) + r] = s_ebase[r];
     }
     __syncthreads();
     uint16_t *sid = S.sid + (size_t)i * W.evcap;
-    for (int t = threadIdx.x; t < N * kCl; t += blockDim.x) {
-        const int s = t / kCl, r = t % kCl;
-        int lo, hi;
-        seg(s, r, lo, hi);
-        uint16_t *dst = sid + s_base[r] + s_len[t];
-        for (int e = lo; e < hi; ++e) dst[e - lo] = (uint16_t)((int)act_k[sk[e]] - r * kClRows);
+    for (int s = tid; s < N; s += kShThreads) {
+        int pos[kCl];
+#pragma unroll
+        for (int r = 0; r < kCl; ++r) pos[r] = s_ebase[r] + s_len[s * kCl + r];
+        for (int e = soff[s]; e < soff[s + 1]; ++e) {
+            const int id = act_k[sk[e]], r = cl_shard(id);
+            int p = 0;
+#pragma unroll
+            for (int q = 0; q < kCl; ++q)
+                if (q == r) p = pos[q]++;
+            sid[p] = (uint16_t)cl_row(id);
+        }
     }
 }
+
+__host__ __device__ inline size_t k_shard_smem(int N) { return (size_t)N * kCl * 4; }
 
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
     k_normad_cl(const TrainArgs T, const ShardWS SW) {
@@ -184,11 +262,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
     __shared__ ClBuf s_buf[2];
     __shared__ int s_abort;
 
-    const int k_lo = r * kClRows, k_hi = min(k_lo + kClRows, kNH);
-    const int rows = k_hi - k_lo;
+    const int rows = cl_rows(r);
     if (T.status[0] != 0) return;  // an earlier chunk failed (uniform over the cluster)
     double *undo = SW.undo + (size_t)r * kClRows * kNO;
-    for (int t = tid; t < rows * kNO; t += kClThreads) Wsh[t] = __ldcg(T.w + (size_t)k_lo * kNO + t);
+    for (int t = tid; t < rows * kNO; t += kClThreads)
+        Wsh[t] = __ldcg(T.w + (size_t)cl_id(r, t / kNO) * kNO + t % kNO);
     if (tid < kCl) flags[tid] = 0;
     const double *SR_lead = cluster.map_shared_rank(SR, 0);
     int *flags_lead = cluster.map_shared_rank(flags, 0);
@@ -203,37 +281,38 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
         uint16_t *sid = reinterpret_cast<uint16_t *>(aoff + (kClACap + 1));
         uint16_t *nsp = sid + kClECap;
         uint16_t *act = nsp + kClECap;
-        const int32_t *sa = SW.act + j * (kCl + 1);
-        const int a0 = sa[r], a1 = sa[r + 1];
-        const int32_t *gaoff = W.act_off + (size_t)j * (kNH + 1);
-        const int e0 = gaoff[a0], e1 = gaoff[a1];
+        const int32_t *ab = SW.abase + j * (kCl + 1), *nb = SW.nbase + j * (kCl + 1);
+        const int a0 = ab[r], na = ab[r + 1] - a0;
+        const int32_t *gaoff = SW.saoff + (size_t)j * (kNH + kCl) + a0 + r;
+        const int ne = gaoff[na];
+        const uint16_t *gact = SW.sact + (size_t)j * kNH + a0;
+        const uint16_t *gnsp = SW.snsp + (size_t)j * W.evcap + nb[r];
         const int32_t *gso = SW.soff + ((size_t)j * kCl + r) * (N + 1);
         const int nid = gso[N];
         const uint16_t *gsid = SW.sid + (size_t)j * W.evcap + SW.ebase[j * (kCl + 1) + r];
-        const bool fa = a1 - a0 <= kClACap && e1 - e0 <= kClECap, fs = nid <= kClECap;
+        const bool fa = na <= kClACap && ne <= kClECap, fs = nid <= kClECap;
         for (int k = t; k <= N; k += nt) soff[k] = gso[k];
         if (fs)
             for (int k = t; k < nid; k += nt) sid[k] = gsid[k];
         if (fa) {
-            for (int k = t; k <= a1 - a0; k += nt) aoff[k] = gaoff[a0 + k];
-            for (int k = t; k < a1 - a0; k += nt) act[k] = W.act_k[(size_t)j * kNH + a0 + k];
-            for (int k = t; k < e1 - e0; k += nt) nsp[k] = W.nsp[(size_t)j * W.evcap + e0 + k];
+            for (int k = t; k <= na; k += nt) aoff[k] = gaoff[k];
+            for (int k = t; k < na; k += nt) act[k] = gact[k];
+            for (int k = t; k < ne; k += nt) nsp[k] = gnsp[k];
         }
         if (t == 0) {
             ClBuf &B = s_buf[b];
             B.soff = soff;
             B.sid = fs ? sid : gsid;
-            B.act = fa ? act : W.act_k + (size_t)j * kNH + a0;
-            B.aoff = fa ? aoff : gaoff + a0;
-            B.nsp = fa ? nsp : W.nsp + (size_t)j * W.evcap + e0;
-            B.abias = fa ? e0 : 0;
-            B.n_act = a1 - a0;
+            B.act = fa ? act : gact;
+            B.aoff = fa ? aoff : gaoff;
+            B.nsp = fa ? nsp : gnsp;
+            B.n_act = na;
         }
     };
     // put back the rows image j changed (undo log)
     auto restore = [&](const ClBuf &B) {
         for (int t = tid; t < B.n_act * kNO; t += kClThreads) {
-            const int row = (int)B.act[t / kNO] - k_lo;
+            const int row = B.act[t / kNO];
             Wsh[row * kNO + t % kNO] = undo[row * kNO + t % kNO];
         }
     };
@@ -356,12 +435,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
         // dW for the shard's active neurons (spikes ascending); commit with an undo log
         bool bad = false;
         for (int a = tid; a < B.n_act; a += kClThreads) {
-            const int row = (int)B.act[a] - k_lo;
+            const int row = B.act[a];
             double acc[kNO];
 #pragma unroll
             for (int l = 0; l < kNO; ++l) acc[l] = 0.0;
-            const int e1 = B.aoff[a + 1] - B.abias;
-            for (int e = B.aoff[a] - B.abias; e < e1; ++e) {
+            const int e1 = B.aoff[a + 1];
+            for (int e = B.aoff[a]; e < e1; ++e) {
                 const double *rr = Rl + (int)B.nsp[e] * kNO;
 #pragma unroll
                 for (int l = 0; l < kNO; ++l) acc[l] = __dadd_rn(acc[l], rr[l]);
@@ -399,7 +478,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
         }
     }
     __syncthreads();
-    for (int t = tid; t < rows * kNO; t += kClThreads) T.w[(size_t)k_lo * kNO + t] = Wsh[t];
+    for (int t = tid; t < rows * kNO; t += kClThreads) T.w[(size_t)cl_id(r, t / kNO) * kNO + t % kNO] = Wsh[t];
     cluster.sync();  // no CTA leaves while others may still read its shared memory
 }
 

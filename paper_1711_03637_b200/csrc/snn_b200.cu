@@ -96,8 +96,8 @@ int64_t train_evcap(const snn_consts_t *c) {
 size_t train_ws_per_image(const snn_consts_t *c) {
     const size_t N = c->n_steps, cap = train_evcap(c);
     return raster_bytes(c, 1) + kMaxTiles * kTile * 2 + 4 + 4 + 4 + kNH * 2 + (kNH + 1) * 4 + cap * 2 +
-           (N + 1) * 4 + cap * 2 + N * 8 + kMaxTiles * N * 8 + 2 * (kCl + 1) * 4 + kCl * (N + 1) * 4 + cap * 2 + N * 8 +
-           (size_t)kCl * kClRows * kNO * 8 / 64;
+           (N + 1) * 4 + cap * 2 + N * 8 + kMaxTiles * N * 8 + 3 * (kCl + 1) * 4 + kCl * (N + 1) * 4 + 2 * cap * 2 +
+           N * 8 + kNH * 2 * 2 + (kNH + kCl) * 4 + (size_t)kCl * kClRows * kNO * 8 / 64;
 }
 
 int64_t train_chunk(const snn_consts_t *c, int64_t n) {
@@ -131,11 +131,16 @@ size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base, 
     w.evcap = (int64_t)cap;
     ShardWS x;
     x.clk = nullptr;
-    x.act = (int32_t *)take(n * (kCl + 1) * 4);
+    x.q = (double *)take(n * N * 8);
     x.soff = (int32_t *)take(n * kCl * (N + 1) * 4);
     x.ebase = (int32_t *)take(n * (kCl + 1) * 4);
     x.sid = (uint16_t *)take(n * cap * 2);
-    x.q = (double *)take(n * N * 8);
+    x.abase = (int32_t *)take(n * (kCl + 1) * 4);
+    x.sact = (uint16_t *)take(n * kNH * 2);
+    x.sidx = (uint16_t *)take(n * kNH * 2);
+    x.saoff = (int32_t *)take(n * (kNH + kCl) * 4);
+    x.nbase = (int32_t *)take(n * (kCl + 1) * 4);
+    x.snsp = (uint16_t *)take(n * cap * 2);
     x.undo = (double *)take((size_t)kCl * kClRows * kNO * 8);
     if (out) *out = w;
     if (sh) *sh = x;
@@ -412,7 +417,7 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
         k_compact<<<(unsigned)cn, kCThreads, 0, s>>>(T);
         if ((rc = cuda_check("k_compact"))) return rc;
         if (use_cl) {
-            k_shard<<<(unsigned)cn, 256, k_shard_smem(c->n_steps), s>>>(T, SW);
+            k_shard<<<(unsigned)cn, kShThreads, k_shard_smem(c->n_steps), s>>>(T, SW);
             if ((rc = cuda_check("k_shard"))) return rc;
             k_normad_cl<<<kCl, kClThreads, cl_smem, s>>>(T, SW);
             if ((rc = cuda_check("k_normad_cl"))) return rc;

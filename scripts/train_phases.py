@@ -32,5 +32,6 @@ print("cycles per phase (median over images 4..63):")
 for i, n in enumerate(names[:11]):
     print(f"  {n:12s} {np.median(d_[:, i]):8.0f}")
 print(f"  {'to next img':12s} {np.median(nxt):8.0f}")
+print("scan cycles per image:", d_[:, 3].tolist())
 tot = np.median(k[1:, 0] - k[:-1, 0])
 print(f"  per image    {tot:8.0f} cycles = {tot / 1.965e3:.2f} us at 1965 MHz")
