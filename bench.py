@@ -199,7 +199,7 @@ def run_reference(args):
     imgs = d["c3_images"]
     cores = host_cores()
     p = orc.Params()
-    sample = int(min(len(imgs), max(2 * cores, cores * 8)))
+    sample = int(min(len(imgs), max(2 * cores, cores * 32)))
     log(f"[reference] oracle port on {cores} cores, {sample} images per step")
     for _ in range(args.warmup):
         orc.batch_counts(imgs[:sample], w, p, workers=cores)
@@ -554,7 +554,7 @@ def cpu_baseline(d, w):
     from oracle import snn_oracle as orc
     cores = host_cores()
     imgs = d["c3_images"]
-    sample = int(min(len(imgs), max(2 * cores, cores * 16)))
+    sample = int(min(len(imgs), max(2 * cores, cores * 64)))   # ~25 core-seconds of CPU work
     p = orc.Params()
     orc.batch_counts(imgs[: 2 * cores], w, p, workers=cores)  # fork + table warm-up
     t0 = time.perf_counter()

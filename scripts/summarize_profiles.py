@@ -87,7 +87,8 @@ def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     run = sys.argv[2] if len(sys.argv) > 2 else None
     os.makedirs(PROF, exist_ok=True)
-    reps = [f"prof_{run}.ncu-rep"] if run else sorted(f for f in os.listdir(OUT) if f.endswith(".ncu-rep"))
+    reps = ([f for f in (f"prof_{run}.ncu-rep", f"prof_train_{run}.ncu-rep") if os.path.exists(os.path.join(OUT, f))]
+            if run else sorted(f for f in os.listdir(OUT) if f.endswith(".ncu-rep")))
     with open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w") as fh:
         fh.write(f"# ncu summary ({tag})\n\nFrom `ncu --set full --clock-control none --import-source on` "
                  "captures (cold-cache, serialised replays: compare shares, not absolutes).\n")
@@ -95,7 +96,8 @@ def main():
             fh.write(f"\n## {rep}\n")
             summarize(os.path.join(OUT, rep), fh)
     if run:
-        for src, dst in ((f"launches_{run}.csv", "launches.csv"), (f"bench_{run}.json", "bench.json")):
+        for src, dst in ((f"launches_{run}.csv", "launches.csv"), (f"launches_train_{run}.csv", "launches_train.csv"),
+                         (f"bench_{run}.json", "bench.json")):
             if os.path.exists(os.path.join(OUT, src)):
                 import shutil
                 shutil.copy(os.path.join(OUT, src), os.path.join(OUT, dst))
