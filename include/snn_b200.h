@@ -128,6 +128,12 @@ void snn_profile_events(void *before, void *after);
  * no gain on one B200 -- the persistent k_hidden leaves no room to overlap). */
 void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_per_sm);
 
+/* The hidden-layer kernel keeps the whole input table in shared memory (one
+ * CTA of 20 warps per SM, no per-chunk barriers) when N <= 108 (enable = 1,
+ * default), else it streams the table through a ring; enable = 0 forces the
+ * ring kernel (same results). */
+void snn_set_hidden_resident(int enable);
+
 /* snn_train runs its sequential NormAD chain on a cluster of 8 CTAs that
  * keeps W in distributed shared memory (default, enable = 1) when N <= ~600,
  * else on one CTA; enable = 0 forces the one-CTA kernel (same results). */

@@ -202,6 +202,22 @@ __host__ __device__ constexpr double def_tap(int f, int k) {
     return (double)def_coef(f, k) * (f < 8 ? kG1 : kG2);
 }
 
+// The distinct tap magnitudes of the default bank, |coef| * gain in IEEE
+// double (2*g1 is an exact doubling, 5*g2 and 4*g2 are numpy's products).
+// Read from the constant bank, so every DFMA takes its tap as an operand
+// (negative taps as a negated operand) instead of re-materialising 64-bit
+// immediates into uniform registers on every step.
+__constant__ double c_def_tap[4] = {kG1, 2.0 * kG1, 5.0 * kG2, 4.0 * kG2};
+
+__host__ __device__ constexpr int def_tap_slot(int f, int k) {
+    return f < 8 ? (def_coef(f, k) == 1 || def_coef(f, k) == -1 ? 0 : 1) : (def_coef(f, k) == 5 ? 2 : 3);
+}
+
+__device__ __forceinline__ double def_tap_c(int f, int k) {
+    const double t = c_def_tap[def_tap_slot(f, k)];
+    return def_coef(f, k) < 0 ? -t : t;
+}
+
 // dgemm's k-ordered FMA chain for a compile-time tap row.  A zero tap adds
 // x*0 = +0 (inputs are >= 0), which leaves the sum unchanged up to the sign
 // of a zero, so skipping it is exact for everything downstream.
@@ -212,7 +228,7 @@ __device__ __forceinline__ double def_current(const double (&x)[9]) {
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
         if (def_coef(F, k) != 0) {
-            I = first ? __dmul_rn(x[k], def_tap(F, k)) : __fma_rn(x[k], def_tap(F, k), I);
+            I = first ? __dmul_rn(x[k], def_tap_c(F, k)) : __fma_rn(x[k], def_tap_c(F, k), I);
             first = false;
         }
     }
@@ -320,11 +336,98 @@ __device__ __forceinline__ unsigned hidden_step(const BatchArgs &A, const LifK &
 // features, which keeps the 54 runtime taps of a warp within the register
 // budget.  The table chunks form one continuous stream across groups, so the
 // TMA ring never drains between groups.
+// One work item's lane state for the whole trial.
+struct ItemState {
+    int64_t img;
+    int tile, pos, nt, half;
+    bool live, on;
+    uint32_t lvp[3];  // the 9 pixel levels of this lane's window, 4 per word
+    uint8_t *rout;    // this lane's raster bytes of chunk 0
+    size_t rstride;   // one chunk of this image
+};
+
+template <bool DEF>
+__device__ __forceinline__ void item_setup(const BatchArgs &A, int item, int total, int nchunks, ItemState &it) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n = A.n_images;
+    it.live = item < total;  // warp-uniform
+    const int gt = DEF ? item : item >> 1;
+    it.half = DEF ? 0 : item & 1;
+    it.img = 0;
+    it.tile = it.pos = it.nt = 0;
+    if (it.live) {
+        int64_t lo = 0, hi = n - 1;  // last image with tile_base <= gt
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (A.tile_base[mid] <= gt) lo = mid;
+            else hi = mid - 1;
+        }
+        it.img = lo;
+        it.tile = gt - A.tile_base[lo];
+        it.nt = A.n_tiles[lo];
+        it.pos = A.tile_pos[lo * (kMaxTiles * kTile) + it.tile * kTile + lane];
+    }
+    it.on = it.live && it.pos != 0xFFFF;
+    const int p = it.on ? it.pos : 0;
+    const int r = p / kFmap, col = p % kFmap;
+    const uint8_t *im = A.images + it.img * (kSide * kSide);
+    it.lvp[0] = it.lvp[1] = it.lvp[2] = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const int k = a * 3 + b;
+            const uint32_t lev = it.on ? __ldg(im + (r + a) * kSide + col + b) : 0u;
+            it.lvp[k >> 2] |= lev << (8 * (k & 3));
+        }
+    it.rout = it.live ? A.raster + raster_tc(A.tile_base[it.img], nchunks, it.nt, 0, it.tile) +
+                            it.half * (kRastTC / 2) + lane * kChunk
+                      : nullptr;
+    it.rstride = (size_t)it.nt * kRastTC;
+}
+
+// The steps of one chunk for one live item (tab = the chunk's [8][256] table
+// rows in shared memory); stores the chunk's raster bytes.
+template <bool TRACE, bool DEF, bool SGN>
+__device__ __forceinline__ void item_chunk(const BatchArgs &A, const LifK &ph, const ItemState &it, const double *tab,
+                                           int ch, double (&v)[kNF], int (&live_from)[kNF]) {
+    const int N = A.c.n_steps;
+    const double refr = A.c.lif_hid.refr;
+    const int s0 = ch * kChunk;
+    const int nrows = min(kChunk, N - s0);
+    uint64_t p0 = 0, p1 = 0;  // the chunk's 6-bit masks, one byte per step
+#pragma unroll 1
+    for (int j = 0; j < nrows; ++j) {
+        const int s = s0 + j;
+        const double *T = tab + j * 256;
+        double x[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) x[k] = T[(it.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu];
+        const int relive = next_live_step(s, refr);
+        unsigned m;
+        if (DEF) m = hidden_step_def<SGN>(ph, x, v, live_from, s, relive);
+        else m = it.half ? hidden_step<1, SGN>(A, ph, x, v, live_from, s, relive)
+                         : hidden_step<0, SGN>(A, ph, x, v, live_from, s, relive);
+        if (TRACE && it.on && A.out.v_hid) {
+            double *dst = A.out.v_hid + ((size_t)it.img * N + s) * kNH + it.pos * kNF + it.half * kHalf;
+#pragma unroll
+            for (int f = 0; f < (DEF ? kNF : kHalf); ++f) dst[f] = v[f];
+        }
+        p0 |= (uint64_t)(m & 0x3Fu) << (8 * j);
+        if (DEF) p1 |= (uint64_t)(m >> kHalf) << (8 * j);
+    }
+    uint64_t *dst = reinterpret_cast<uint64_t *>(it.rout + (size_t)ch * it.rstride);
+    dst[0] = p0;
+    if (DEF) dst[kTile] = p1;  // the second half plane, 256 bytes on
+}
+
+// Ring variant: the table streams through a 2-stage ring shared by the CTA's
+// warps, which therefore step through the chunks together (any N).
 template <bool TRACE, bool DEF, bool SGN>
 __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
     __shared__ __align__(128) double s_tab[kStages][kChunk * 256];
     __shared__ uint64_t s_full[kStages];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5;
     const int N = A.c.n_steps;
     const int nchunks = (N + kChunk - 1) / kChunk;
     const int64_t n = A.n_images;
@@ -348,43 +451,13 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
     }
     __syncthreads();
 
-    const double el = A.c.lif_hid.el, refr = A.c.lif_hid.refr;
+    const double el = A.c.lif_hid.el;
     const LifK ph = lif_k(A.c.lif_hid);
     int64_t q = 0;
     for (int gi = 0; gi < my_groups; ++gi) {
         const int item = ((int)blockIdx.x + gi * (int)gridDim.x) * kWPC + warp;
-        const bool live = item < total;  // warp-uniform
-        const int gt = DEF ? item : item >> 1, half = DEF ? 0 : item & 1;
-        int64_t img = 0;
-        int tile = 0, pos = 0, nt = 0;
-        if (live) {
-            int64_t lo = 0, hi = n - 1;  // last image with tile_base <= gt
-            while (lo < hi) {
-                const int64_t mid = (lo + hi + 1) >> 1;
-                if (A.tile_base[mid] <= gt) lo = mid;
-                else hi = mid - 1;
-            }
-            img = lo;
-            tile = gt - A.tile_base[img];
-            nt = A.n_tiles[img];
-            pos = A.tile_pos[img * (kMaxTiles * kTile) + tile * kTile + lane];
-        }
-        const bool on = live && pos != 0xFFFF;
-        uint32_t lvp[3];  // the 9 pixel levels of this lane's window, 4 per word
-        {
-            const int p = on ? pos : 0;
-            const int r = p / kFmap, col = p % kFmap;
-            const uint8_t *im = A.images + img * (kSide * kSide);
-            lvp[0] = lvp[1] = lvp[2] = 0;
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) {
-                    const int k = a * 3 + b;
-                    const uint32_t lev = on ? __ldg(im + (r + a) * kSide + col + b) : 0u;
-                    lvp[k >> 2] |= lev << (8 * (k & 3));
-                }
-        }
+        ItemState it;
+        item_setup<DEF>(A, item, total, nchunks, it);
         double v[kNF];
         int live_from[kNF];
 #pragma unroll
@@ -392,45 +465,60 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
             v[f] = el;
             live_from[f] = 0;
         }
-        uint8_t *rout = live ? A.raster + raster_tc(A.tile_base[img], nchunks, nt, 0, tile) + half * (kRastTC / 2) +
-                                   lane * kChunk
-                             : nullptr;
-        const size_t rstride = (size_t)nt * kRastTC;  // one chunk of this image
-
         for (int ch = 0; ch < nchunks; ++ch, ++q) {
             const int b = (int)(q % kStages);
-            const int s0 = ch * kChunk;
-            const int nrows = min(kChunk, N - s0);
-            if (live) {
+            if (it.live) {
                 mbar_wait(&s_full[b], (uint32_t)((q / kStages) & 1));
-                uint64_t p0 = 0, p1 = 0;  // the chunk's 6-bit masks, one byte per step
-#pragma unroll 1
-                for (int j = 0; j < nrows; ++j) {
-                    const int s = s0 + j;
-                    const double *T = s_tab[b] + j * 256;
-                    double x[9];
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) x[k] = T[(lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu];
-                    const int relive = next_live_step(s, refr);
-                    unsigned m;
-                    if (DEF) m = hidden_step_def<SGN>(ph, x, v, live_from, s, relive);
-                    else m = half ? hidden_step<1, SGN>(A, ph, x, v, live_from, s, relive)
-                                  : hidden_step<0, SGN>(A, ph, x, v, live_from, s, relive);
-                    if (TRACE && on && A.out.v_hid) {
-                        double *dst = A.out.v_hid + ((size_t)img * N + s) * kNH + pos * kNF + half * kHalf;
-#pragma unroll
-                        for (int f = 0; f < (DEF ? kNF : kHalf); ++f) dst[f] = v[f];
-                    }
-                    p0 |= (uint64_t)(m & 0x3Fu) << (8 * j);
-                    if (DEF) p1 |= (uint64_t)(m >> kHalf) << (8 * j);
-                }
-                uint64_t *dst = reinterpret_cast<uint64_t *>(rout + (size_t)ch * rstride);
-                dst[0] = p0;
-                if (DEF) dst[kTile] = p1;  // the second half plane, 256 bytes on
+                item_chunk<TRACE, DEF, SGN>(A, ph, it, s_tab[b], ch, v, live_from);
             }
             __syncthreads();  // every warp is done with stage b
             if (tid == 0 && q + kStages < stream_len) issue(q + kStages);
         }
+    }
+}
+
+// Resident variant (N <= kResMaxSteps): one CTA of kResWarps warps per SM holds
+// the whole [N][256] table in shared memory (one bulk load), so its warps run
+// their items independently -- no ring, no per-chunk barrier.
+constexpr int kResWarps = 20;
+constexpr int kResMaxSteps = 108;  // 108 * 2 KB = 216 KB of table
+
+template <bool TRACE, bool DEF, bool SGN>
+__global__ void __launch_bounds__(kResWarps * 32, 1) k_hidden_res(const BatchArgs A) {
+    extern __shared__ __align__(128) double r_tab[];
+    __shared__ uint64_t r_full;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int N = A.c.n_steps;
+    const int nchunks = (N + kChunk - 1) / kChunk;
+    const int64_t n = A.n_images;
+    constexpr int kItemsPerTile = DEF ? 1 : 2;
+    const int total = kItemsPerTile * A.tile_base[n];
+    if (tid == 0) {
+        mbar_init(&r_full, 1);
+        fence_mbar_init();
+        mbar_expect_tx(&r_full, (uint32_t)N * 256 * 8);
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int rows = min(kChunk, N - ch * kChunk);
+            bulk_g2s(r_tab + (size_t)ch * kChunk * 256, A.ctab + (size_t)ch * kChunk * 256, rows * 256 * 8, &r_full);
+        }
+    }
+    __syncthreads();
+    mbar_wait(&r_full, 0);
+    const double el = A.c.lif_hid.el;
+    const LifK ph = lif_k(A.c.lif_hid);
+    const int stride = (int)gridDim.x * kResWarps;
+    for (int item = (int)blockIdx.x * kResWarps + warp; item < total; item += stride) {
+        ItemState it;
+        item_setup<DEF>(A, item, total, nchunks, it);
+        double v[kNF];
+        int live_from[kNF];
+#pragma unroll
+        for (int f = 0; f < kNF; ++f) {
+            v[f] = el;
+            live_from[f] = 0;
+        }
+        for (int ch = 0; ch < nchunks; ++ch)
+            item_chunk<TRACE, DEF, SGN>(A, ph, it, r_tab + (size_t)ch * kChunk * 256, ch, v, live_from);
     }
 }
 

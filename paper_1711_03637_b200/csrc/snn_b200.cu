@@ -162,6 +162,7 @@ int sm_count() {
 
 // k_hidden CTAs per SM (0 = occupancy limit); snn_set_pipeline
 int g_hid_ctas = 0;
+int g_hid_res = 1;  // snn_set_hidden_resident
 int g_normad_cluster = 1;  // snn_set_normad_cluster
 long long *g_phase_clk = nullptr;  // snn_normad_phase_clocks
 int64_t g_pipe_images = 0;
@@ -183,10 +184,24 @@ int launch_hidden(const BatchArgs &A, cudaStream_t st) {
     if ((rc = cuda_check("k_prep"))) return rc;
     k_tile_scan<<<1, 1024, 0, st>>>(A);
     if ((rc = cuda_check("k_tile_scan"))) return rc;
-    const int64_t max_groups = (2 * A.n_images * kMaxTiles + kWPC - 1) / kWPC;
-    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)per_sm * sm_count(), max_groups);
     if (g_ev_before) cudaEventRecord(g_ev_before, st);
-    k_hidden<TRACE, DEF, SGN><<<grid, kThreads, 0, st>>>(A);
+    if (g_hid_res && A.c.n_steps <= kResMaxSteps) {  // table resident in shared memory
+        static bool attr = false;
+        const size_t smem = (size_t)A.c.n_steps * 256 * 8;
+        if (!attr) {
+            if (cudaFuncSetAttribute(k_hidden_res<TRACE, DEF, SGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(kResMaxSteps * 256 * 8)) != cudaSuccess)
+                return cuda_check("cudaFuncSetAttribute(k_hidden_res)");
+            attr = true;
+        }
+        const int64_t max_ctas = (2 * A.n_images * kMaxTiles + kResWarps - 1) / kResWarps;
+        const unsigned grid = (unsigned)std::min<int64_t>(sm_count(), max_ctas);
+        k_hidden_res<TRACE, DEF, SGN><<<grid, kResWarps * 32, smem, st>>>(A);
+    } else {
+        const int64_t max_groups = (2 * A.n_images * kMaxTiles + kWPC - 1) / kWPC;
+        const unsigned grid = (unsigned)std::min<int64_t>((int64_t)per_sm * sm_count(), max_groups);
+        k_hidden<TRACE, DEF, SGN><<<grid, kThreads, 0, st>>>(A);
+    }
     if ((rc = cuda_check("k_hidden"))) return rc;
     if (g_ev_after) cudaEventRecord(g_ev_after, st);
     return SNN_OK;
@@ -346,6 +361,8 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
 }
 
 extern "C" void snn_set_normad_cluster(int enable) { g_normad_cluster = enable; }
+
+extern "C" void snn_set_hidden_resident(int enable) { g_hid_res = enable; }
 
 extern "C" void snn_normad_phase_clocks(long long *d_clk) { g_phase_clk = d_clk; }
 

@@ -353,3 +353,36 @@ def test_c5_full_pass_vs_reference(sd, cfg, bank):
     same_ev = float((ev == g["eval_counts_500"]).all(axis=1).mean())
     assert same_ev >= 0.999
     assert np.mean(np.argmax(ev, 1) == np.argmax(g["eval_counts_500"], 1)) >= 0.999
+
+
+def test_hidden_kernel_variants_identical(sd, cfg, bank, workloads, wfix):
+    """The table-resident and the ring-streamed hidden-layer kernels give the
+    same bits (snn_set_hidden_resident), and so does the one-CTA NormAD kernel
+    vs the cluster kernel (snn_set_normad_cluster)."""
+    from paper_1711_03637_b200.engine import get_engine, make_consts
+    eng = get_engine()
+    c = make_consts(cfg, bank)
+    imgs = torch.from_numpy(workloads["c3_images"][:64].reshape(64, -1).copy()).to(eng.device)
+    w = torch.from_numpy(wfix["w_fix"].copy()).to(eng.device)
+    outs = []
+    for res in (1, 0):
+        eng.lib.snn_set_hidden_resident(res)
+        try:
+            o = eng.infer(c, imgs, w, trace=True)
+            outs.append({k: o[k].cpu().numpy() for k in ("counts", "ff", "v_out")})
+        finally:
+            eng.lib.snn_set_hidden_resident(1)
+    for k in outs[0]:
+        assert np.array_equal(outs[0][k], outs[1][k]), k
+    learn = sd.LearnConfig()
+    order = workloads["c2_order"][:40]
+    ims, labs = workloads["c2_images"][order], workloads["c2_labels"][order]
+    res = []
+    for cl in (1, 0):
+        eng.lib.snn_set_normad_cluster(cl)
+        try:
+            res.append(sd.train_epoch(ims, labs, sd.zero_weights(), bank, cfg, learn)[0])
+        finally:
+            eng.lib.snn_set_normad_cluster(1)
+    rel = np.abs(res[0] - res[1]).max() / np.abs(res[1]).max()
+    assert rel <= 1e-12, rel   # G summed per shard vs sequentially: last-bit differences only
