@@ -627,14 +627,12 @@ __device__ __forceinline__ bool out_step(OutState &st, const snn_consts_t &c, do
 // order, so results never depend on the batch an image is in.  One warp per
 // (image, 8-step chunk); chunks are independent, so a single image spreads
 // over ceil(N/8) warps.
-//   lists  per tile (in order): each lane counts its window's spikes per step;
-//          one packed warp scan gives per-lane offsets (8-bit fields when the
-//          tile-chunk has at most 255 spikes, else 16-bit).  Then the warp
-//          fills the tile's list slots 32 at a time: slot -> step (prefix of
-//          step totals) -> owning lane (binary search over the offsets in
-//          shared memory) -> bit of that lane's mask.  No divergent loops.
-//          Tiles ascend in window position, lanes within a tile too and
-//          features within a lane: every step list is in ascending neuron id.
+//   lists  per tile (in order) the warp is transposed: lane (j, g) takes step j
+//          of the tile's windows 8g .. 8g+7 (masks staged in shared memory),
+//          counts their spikes, a 4-lane prefix gives its offset in step j's
+//          list, and it writes their neuron ids.  Tiles ascend in window
+//          position, windows within a tile too and features within a window:
+//          every step list is in ascending neuron id.
 //   sums   lane (j, p) walks step j's list for outputs 2p, 2p+1 (16-byte W
 //          loads, 8 in flight).  A step with more than kStepCap spikes is
 //          summed afterwards tile by tile, in the same order.
@@ -665,8 +663,7 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t x) {
 struct GsumSmem {
     uint16_t ids[kChunk * kStepCap];  // the chunk's step lists
     uint16_t pos[kMaxTiles * kTile];  // window position of each (tile, lane)
-    uint16_t off[kTile * kChunk];     // [lane][step] exclusive offsets within the tile
-    uint16_t msk[kTile * kChunk];     // [lane][step] 12-bit spike masks
+    uint64_t pl[2][kTile];            // the current tile's two mask planes, per window
 };
 
 __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double *G) {
@@ -683,93 +680,70 @@ __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double
     for (int k = lane; k < nt * kTile; k += 32) S.pos[k] = A.tile_pos[img * (kMaxTiles * kTile) + k];
     const uint8_t *R = A.raster + raster_tc(A.tile_base[img], nch, nt, ch, 0) + lane * kChunk;
     const double *W = A.w;
-    uint32_t run[kChunk];  // list lengths so far (warp-uniform)
-#pragma unroll
-    for (int j = 0; j < kChunk; ++j) run[j] = 0;
-    // the next tile's masks are loaded while this tile's list is built
-    uint2 n0 = make_uint2(0, 0), n1 = make_uint2(0, 0);
+    // ---- lists: lane (jl, g) = (step, window group of 8)
+    const int jl = lane >> 2, g = lane & 3;
+    uint32_t runl = 0;  // step jl's list length so far
+    uint64_t n0 = 0, n1 = 0;  // the next tile's planes, loaded ahead
     if (nt > 0) {
-        n0 = __ldcs(reinterpret_cast<const uint2 *>(R));
-        n1 = __ldcs(reinterpret_cast<const uint2 *>(R + kRastTC / 2));
+        n0 = __ldcs(reinterpret_cast<const unsigned long long *>(R));
+        n1 = __ldcs(reinterpret_cast<const unsigned long long *>(R + kRastTC / 2));
     }
-    __syncwarp();
+    const uint8_t *b0 = reinterpret_cast<const uint8_t *>(S.pl[0]) + jl, *b1 = reinterpret_cast<const uint8_t *>(S.pl[1]) + jl;
     for (int t = 0; t < nt; ++t) {
-        const uint2 a0 = n0, a1 = n1;
+        __syncwarp();
+        S.pl[0][lane] = n0;
+        S.pl[1][lane] = n1;
+        const bool any = __any_sync(kFull, (n0 | n1) != 0ull);
         if (t + 1 < nt) {
             const uint8_t *nxt = R + (size_t)(t + 1) * kRastTC;
-            n0 = __ldcs(reinterpret_cast<const uint2 *>(nxt));
-            n1 = __ldcs(reinterpret_cast<const uint2 *>(nxt + kRastTC / 2));
+            n0 = __ldcs(reinterpret_cast<const unsigned long long *>(nxt));
+            n1 = __ldcs(reinterpret_cast<const unsigned long long *>(nxt + kRastTC / 2));
         }
-        const uint32_t clo = byte_popc(a0.x) + byte_popc(a1.x);  // steps 0..3, one byte each (<= 12)
-        const uint32_t chi = byte_popc(a0.y) + byte_popc(a1.y);  // steps 4..7
-        const unsigned tot = __reduce_add_sync(kFull, ((clo * 0x01010101u) >> 24) + ((chi * 0x01010101u) >> 24));
-        if (tot == 0) continue;  // warp-uniform: no spike in this tile-chunk
-        uint4 ow, tw;            // exclusive offsets / tile totals, 16-bit fields, steps (0,1) (2,3) (4,5) (6,7)
-        if (tot <= 255) {        // one scan: 8-bit fields cannot overflow
-            const uint64_t c8 = ((uint64_t)chi << 32) | clo;
-            const uint64_t inc = warp_incl_scan_u64(c8);
-            const uint64_t exc = inc - c8;
-            const uint64_t tt = __shfl_sync(kFull, inc, 31);
-            ow = make_uint4(__byte_perm((uint32_t)exc, 0, 0x4140), __byte_perm((uint32_t)exc, 0, 0x4342),
-                            __byte_perm((uint32_t)(exc >> 32), 0, 0x4140), __byte_perm((uint32_t)(exc >> 32), 0, 0x4342));
-            tw = make_uint4(__byte_perm((uint32_t)tt, 0, 0x4140), __byte_perm((uint32_t)tt, 0, 0x4342),
-                            __byte_perm((uint32_t)(tt >> 32), 0, 0x4140), __byte_perm((uint32_t)(tt >> 32), 0, 0x4342));
-        } else {
-            const uint64_t cA = ((uint64_t)__byte_perm(clo, 0, 0x4342) << 32) | __byte_perm(clo, 0, 0x4140);
-            const uint64_t cB = ((uint64_t)__byte_perm(chi, 0, 0x4342) << 32) | __byte_perm(chi, 0, 0x4140);
-            const uint64_t iA = warp_incl_scan_u64(cA), iB = warp_incl_scan_u64(cB);
-            const uint64_t eA = iA - cA, eB = iB - cB;
-            const uint64_t tA = __shfl_sync(kFull, iA, 31), tB = __shfl_sync(kFull, iB, 31);
-            ow = make_uint4((uint32_t)eA, (uint32_t)(eA >> 32), (uint32_t)eB, (uint32_t)(eB >> 32));
-            tw = make_uint4((uint32_t)tA, (uint32_t)(tA >> 32), (uint32_t)tB, (uint32_t)(tB >> 32));
-        }
-        reinterpret_cast<uint4 *>(S.off)[lane] = ow;
-        reinterpret_cast<uint4 *>(S.msk)[lane] =
-            make_uint4(__byte_perm(a0.x, 0, 0x4140) | (__byte_perm(a1.x, 0, 0x4140) << kHalf),
-                       __byte_perm(a0.x, 0, 0x4342) | (__byte_perm(a1.x, 0, 0x4342) << kHalf),
-                       __byte_perm(a0.y, 0, 0x4140) | (__byte_perm(a1.y, 0, 0x4140) << kHalf),
-                       __byte_perm(a0.y, 0, 0x4342) | (__byte_perm(a1.y, 0, 0x4342) << kHalf));
-        const uint32_t T[kChunk] = {tw.x & 0xFFFFu, tw.x >> 16, tw.y & 0xFFFFu, tw.y >> 16,
-                                    tw.z & 0xFFFFu, tw.z >> 16, tw.w & 0xFFFFu, tw.w >> 16};
+        if (!any) continue;  // warp-uniform: no spike in this tile-chunk
         __syncwarp();
-        for (unsigned k0 = 0; k0 < tot; k0 += 32) {
-            const unsigned k = k0 + lane;
-            if (k < tot) {
-                // step of slot k: steps are laid out one after another
-                int j = 0;
-                unsigned sj = 0, acc = 0, base = run[0];
+        unsigned m[8];
+        unsigned cnt = 0;
 #pragma unroll
-                for (int jj = 0; jj < kChunk; ++jj) {
-                    if (k >= acc) {
-                        j = jj;
-                        sj = acc;
-                        base = run[jj];
-                    }
-                    acc += T[jj];
-                }
-                const unsigned q = k - sj;  // rank within the tile's step-j list
-                int L = 0;                  // owning lane: largest L with off[L][j] <= q
-#pragma unroll
-                for (int st = 16; st > 0; st >>= 1)
-                    if (S.off[(L + st) * kChunk + j] <= q) L += st;
-                unsigned m = S.msk[L * kChunk + j];
-                for (unsigned r = q - S.off[L * kChunk + j]; r; --r) m &= m - 1u;
-                const unsigned slot = base + q;
-                if (slot < kStepCap) S.ids[j * kStepCap + slot] = (uint16_t)(S.pos[t * kTile + L] * kNF + __ffs(m) - 1);
-            }
+        for (int i = 0; i < 8; ++i) {
+            const int w = g * 8 + i;
+            m[i] = (unsigned)b0[w * 8] | ((unsigned)b1[w * 8] << kHalf);
+            cnt += __popc(m[i]);
         }
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) run[j] += T[j];
-        __syncwarp();
+        // prefix over the 4 window groups of step jl
+        unsigned inc = cnt;
+        unsigned y = __shfl_up_sync(kFull, inc, 1);
+        if (g >= 1) inc += y;
+        y = __shfl_up_sync(kFull, inc, 2);
+        if (g >= 2) inc += y;
+        const unsigned tot = __shfl_sync(kFull, inc, lane | 3);
+        unsigned k = runl + inc - cnt;
+        uint16_t *dst = S.ids + jl * kStepCap;
+        const uint16_t *tp = S.pos + t * kTile + g * 8;
+        // one loop over all of this lane's spikes: 12-bit fields of windows 0..4 and 5..7
+        uint64_t w0 = (uint64_t)m[0] | ((uint64_t)m[1] << 12) | ((uint64_t)m[2] << 24) | ((uint64_t)m[3] << 36) |
+                      ((uint64_t)m[4] << 48);
+        uint64_t w1 = (uint64_t)m[5] | ((uint64_t)m[6] << 12) | ((uint64_t)m[7] << 24);
+        while (w0 | w1) {
+            const bool lo = w0 != 0ull;
+            const uint64_t w = lo ? w0 : w1;
+            const int b = __ffsll((long long)w) - 1 + (lo ? 0 : 60);
+            if (lo) w0 &= w0 - 1ull;
+            else w1 &= w1 - 1ull;
+            const int i = (b * 43) >> 9;  // b / 12 for b < 96
+            if (k < (unsigned)kStepCap) dst[k] = (uint16_t)((int)tp[i] * kNF + (b - 12 * i));
+            ++k;
+        }
+        runl += tot;
     }
+    __syncwarp();
+    // steps whose list overflowed kStepCap (bit j), warp-uniform
+    const unsigned ovf = __ballot_sync(kFull, g == 0 && runl > (uint32_t)kStepCap) ;
     // ---- sums: lane (j, p) -> G[j][2p], G[j][2p+1]; rounds of 6 steps
     double *Gi = G + ((size_t)img * N + s0) * kNO;
 #pragma unroll 1
     for (int j0 = 0; j0 < ns; j0 += 6) {
         const int j = j0 + lane / 5, p = lane % 5;
-        unsigned cnt = 0;
-#pragma unroll
-        for (int jj = 0; jj < kChunk; ++jj) cnt = jj == j ? run[jj] : cnt;
+        const unsigned cnt = __shfl_sync(kFull, runl, (j & 7) * 4);
         if (lane < 30 && j < ns && cnt <= kStepCap) {
             const uint16_t *lst = S.ids + j * kStepCap;
             const double2 *W2 = reinterpret_cast<const double2 *>(W) + p;
@@ -794,12 +768,8 @@ __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double
         }
     }
     // rare: a step with more than kStepCap spikes -- same order, tile by tile
-#pragma unroll 1
-    for (int j = 0; j < ns; ++j) {
-        unsigned cnt = 0;
-#pragma unroll
-        for (int jj = 0; jj < kChunk; ++jj) cnt = jj == j ? run[jj] : cnt;
-        if (cnt <= kStepCap) continue;  // warp-uniform
+    for (unsigned ov = ovf; ov; ov &= ov - 1u) {
+        const int j = (__ffs(ov) - 1) >> 2;
         __syncwarp();
         double g = 0.0;
         for (int t = 0; t < nt; ++t) {

@@ -67,6 +67,7 @@ struct ShardWS {
     int32_t *nbase;   // [n][kCl + 1]      start of each shard's spike block in snsp
     uint16_t *snsp;   // [n][evcap]        shard-major spike steps of the active neurons
     double *undo;     // [kCl][kClRows][10] old rows of the last committed image
+    int push;         // partials / R pushed through DSMEM stores (normad_cl_smem_bytes)
 };
 
 // one image's lists of one shard, staged (or pointing into global memory
@@ -84,12 +85,16 @@ __host__ __device__ inline size_t cl_buf_bytes(int N) {
     return (size_t)(N + 1) * 4 + (size_t)(kClACap + 1) * 4 + (size_t)kClECap * 2 * 2 + (size_t)kClACap * 2 + 16;
 }
 
-__host__ __device__ inline size_t normad_cl_smem_bytes(int N) {
+// push: every CTA stores its G partials straight into the leader's shared
+// memory (and the leader stores R into every CTA's), so no CTA reads remote
+// shared memory on the serial path; needs kCl partial buffers on the leader.
+__host__ __device__ inline size_t normad_cl_smem_bytes(int N, bool push) {
     return (size_t)kClRows * kNO * 8          // W shard
-           + (size_t)N * kNO * 8 * 3          // P (G on the leader), R copy, sigma / R (leader)
+           + (size_t)N * kNO * 8 * 3          // P (G on the leader), R copy, R (leader)
            + (size_t)N * 8                    // q (leader)
            + (size_t)N * 2 + 64 + 16          // OMASK, flags
-           + 2 * ((cl_buf_bytes(N) + 15) & ~(size_t)15);
+           + 2 * ((cl_buf_bytes(N) + 15) & ~(size_t)15)
+           + (push ? (size_t)kCl * N * kNO * 8 : 0);  // the partials of every CTA (leader)
 }
 
 // k_shard: grid = images.  dt / |d_hat(s)|, and the image's active neurons,
@@ -259,6 +264,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
     int *flags = reinterpret_cast<int *>(OMASK + ((N + 7) & ~7));  // leader: per-CTA non-finite flags
     uint8_t *bufmem = reinterpret_cast<uint8_t *>(flags + 16);
     const size_t bstride = (cl_buf_bytes(N) + 15) & ~(size_t)15;
+    double *PQ = reinterpret_cast<double *>(bufmem + 2 * bstride);  // leader, push: [kCl][N][10]
+    const bool push = SW.push != 0;
     __shared__ ClBuf s_buf[2];
     __shared__ int s_abort;
 
@@ -269,6 +276,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
         Wsh[t] = __ldcg(T.w + (size_t)cl_id(r, t / kNO) * kNO + t % kNO);
     if (tid < kCl) flags[tid] = 0;
     const double *SR_lead = cluster.map_shared_rank(SR, 0);
+    double *PQ_lead = cluster.map_shared_rank(PQ, 0) + (size_t)r * N * kNO;  // this CTA's partials there
     int *flags_lead = cluster.map_shared_rank(flags, 0);
 
     // stage image j's lists of this shard into buffer b with threads [t0, t0 + nt)
@@ -343,7 +351,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
                 for (int u = 0; u < 4; ++u) g = __dadd_rn(g, Wsh[id[u] * kNO + l]);
             }
             for (; e < e1; ++e) g = __dadd_rn(g, Wsh[(int)B.sid[e] * kNO + l]);
-            P[t] = g;
+            if (push) PQ_lead[t] = g;
+            else P[t] = g;
         }
         stamp(1);
         cluster.sync();  // B1: partials ready, flags of image i-1 published
@@ -371,8 +380,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
             for (int t = tid; t < N * kNO; t += kClThreads) {
                 double v[kCl];
 #pragma unroll
-                for (int q = 1; q < kCl; ++q) v[q] = cluster.map_shared_rank(P, q)[t];
-                double g = P[t];
+                for (int q = 0; q < kCl; ++q)
+                    v[q] = push ? PQ[(size_t)q * N * kNO + t] : (q ? cluster.map_shared_rank(P, q)[t] : P[t]);
+                double g = v[0];
 #pragma unroll
                 for (int q = 1; q < kCl; ++q) g = __dadd_rn(g, v[q]);
                 P[t] = g;
@@ -396,17 +406,18 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
             }
             __syncthreads();
             stamp(4);
-            // error signal and gate (normad.py:156-159, :87-91, :104-113): the
-            // step counts when some e != 0 and |d_hat| > eps; sigma = e * dt / |d_hat|
+            // error signal and gate (normad.py:156-159, :87-91, :104-113): the step
+            // counts when some e != 0 and |d_hat| > eps; sigma = e * dt / |d_hat| =
+            // +-(dt / |d_hat|) (IEEE division is sign-symmetric)
             {
                 const int label = T.labels[i];
                 const int per = c.desired_period;
                 for (int t = tid; t < N * kNO; t += kClThreads) {
                     const int s = t / kNO, l = t - s * kNO;
-                    const bool want = per > 0 && s >= per - 1 && (s - (per - 1)) % per == 0 && l == label;
+                    const bool want = per > 0 && (s + 1) % per == 0 && l == label;  // network.py:191-193
                     const bool got = (OMASK[s] >> l) & 1u;
                     const double q = Q[s];
-                    SR[t] = want == got ? 0.0 : (want ? q : -q);  // (+-dt) / |d_hat| == +-(dt / |d_hat|)
+                    SR[t] = want == got ? 0.0 : (want ? q : -q);
                 }
             }
             __syncthreads();
@@ -424,13 +435,20 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
             }
             __syncthreads();
             stamp(6);
+            if (push)  // R into every CTA's shared memory
+                for (int t = tid; t < kCl * N * kNO; t += kClThreads) {
+                    const int q = t / (N * kNO), k = t - q * (N * kNO);
+                    cluster.map_shared_rank(Rl, q)[k] = SR[k];
+                }
         } else if (more) {
             stage(i + 1, (int)((i + 1) & 1), 0, kClThreads);
         }
         cluster.sync();  // B2: R ready on the leader, next lists staged
         stamp(7);
-        for (int t = tid; t < N * kNO; t += kClThreads) Rl[t] = SR_lead[t];
-        __syncthreads();
+        if (!push) {
+            for (int t = tid; t < N * kNO; t += kClThreads) Rl[t] = SR_lead[t];
+            __syncthreads();
+        }
         stamp(8);
         // dW for the shard's active neurons (spikes ascending); commit with an undo log
         bool bad = false;

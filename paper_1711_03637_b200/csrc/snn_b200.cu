@@ -390,7 +390,8 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     if (((uintptr_t)d_images & 15) != 0) return set_error(SNN_EINVAL, "images must be 16-byte aligned");
     if (c->n_steps > 65535) return set_error(SNN_EINVAL, "training supports n_steps <= 65535");
     // the W-resident cluster kernel when its shared memory fits, else the one-CTA kernel
-    const size_t cl_smem = normad_cl_smem_bytes(c->n_steps);
+    const bool cl_push = g_normad_cluster == 1 && normad_cl_smem_bytes(c->n_steps, true) <= 227 * 1024;
+    const size_t cl_smem = normad_cl_smem_bytes(c->n_steps, cl_push);
     const bool use_cl = g_normad_cluster && cl_smem <= 227 * 1024;
     const NormadCaps caps = normad_caps(c);
     const size_t smem = normad_smem_bytes(c->n_steps, caps);
@@ -401,6 +402,7 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     ShardWS SW;
     const size_t need = train_ws(c, chunk, &T.ws, (char *)d_ws, &SW);
     SW.clk = g_phase_clk;
+    SW.push = cl_push ? 1 : 0;
     if (!d_ws || ws_bytes < need) return set_error(SNN_ENOMEM, "workspace too small");
     if (use_cl) {
         if (cudaFuncSetAttribute(k_normad_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem) != cudaSuccess)
