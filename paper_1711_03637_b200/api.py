@@ -96,15 +96,37 @@ def _replay_hook(on_step: Callable, hidden: np.ndarray, out_mask: np.ndarray, dt
         on_step(n, a - b, out_mask[n].copy())
 
 
+_CONSTS_CACHE: dict = {}
+
+
+def _consts_cached(cfg, filters):
+    """make_consts for the serving path, cached on (config, filter taps)."""
+    try:
+        key = (cfg, np.asarray(filters.weighted, dtype=np.float64).tobytes())
+        hit = _CONSTS_CACHE.get(key)
+    except TypeError:  # unhashable config object
+        return make_consts(cfg, filters)
+    if hit is None:
+        if len(_CONSTS_CACHE) > 64:
+            _CONSTS_CACHE.clear()
+        hit = _CONSTS_CACHE[key] = make_consts(cfg, filters)
+    return hit
+
+
 def run_presentation(image, weights, filters, cfg,
                      on_step: Optional[Callable[[int, np.ndarray, np.ndarray], None]] = None,
                      _record_into: Optional[dict] = None) -> np.ndarray:
     """Simulate one image for T/dt steps on the GPU; returns int64[10] counts."""
-    w = _weights(weights)
-    img = as_pixel_image(image)
-    c = make_consts(cfg, filters)
     eng = get_engine()
     record = on_step is not None or _record_into is not None
+    if not record:  # the serving path: cached device weights, one CUDA-graph launch
+        with eng.lock:
+            eng.weights(weights, check=_weights)  # validated first, as network.py:280 does
+            img = as_pixel_image(image)
+            return eng.infer_one(_consts_cached(cfg, filters), img)
+    w = _weights(weights)
+    img = as_pixel_image(image)
+    c = _consts_cached(cfg, filters)
     with eng.lock:
         d_img = _to_device(eng, img.reshape(1, -1))
         d_w = _to_device(eng, w)

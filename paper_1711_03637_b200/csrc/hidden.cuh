@@ -506,8 +506,9 @@ __global__ void __launch_bounds__(kResWarps * 32, 1) k_hidden_res(const BatchArg
     mbar_wait(&r_full, 0);
     const double el = A.c.lif_hid.el;
     const LifK ph = lif_k(A.c.lif_hid);
+    // items interleaved over the CTAs, so a small batch spreads over many SMs
     const int stride = (int)gridDim.x * kResWarps;
-    for (int item = (int)blockIdx.x * kResWarps + warp; item < total; item += stride) {
+    for (int item = warp * (int)gridDim.x + (int)blockIdx.x; item < total; item += stride) {
         ItemState it;
         item_setup<DEF>(A, item, total, nchunks, it);
         double v[kNF];

@@ -194,8 +194,8 @@ int launch_hidden(const BatchArgs &A, cudaStream_t st) {
                 return cuda_check("cudaFuncSetAttribute(k_hidden_res)");
             attr = true;
         }
-        const int64_t max_ctas = (2 * A.n_images * kMaxTiles + kResWarps - 1) / kResWarps;
-        const unsigned grid = (unsigned)std::min<int64_t>(sm_count(), max_ctas);
+        const int64_t max_items = (int64_t)A.items_per_tile * A.n_images * kMaxTiles;
+        const unsigned grid = (unsigned)std::min<int64_t>(sm_count(), max_items);
         k_hidden_res<TRACE, DEF, SGN><<<grid, kResWarps * 32, smem, st>>>(A);
     } else {
         const int64_t max_groups = (2 * A.n_images * kMaxTiles + kWPC - 1) / kWPC;

@@ -79,6 +79,9 @@ class Engine:
         self.lock = threading.RLock()
         self._tables: dict = {}
         self._ws: dict = {}
+        self._w_host = None      # host copy of the weights last uploaded by weights()
+        self._w_dev = None
+        self._graphs: dict = {}  # batch-1 CUDA graphs per configuration (infer_one)
 
     # ------------------------------------------------------------ helpers
     @property
@@ -155,6 +158,65 @@ class Engine:
                 ctypes.byref(o), ws.data_ptr(), ws_bytes, self.sptr))
         torch.cuda.current_stream(dev).wait_stream(self.stream)   # results safe on the caller's stream
         return out
+
+    # ------------------------------------------------------------ serving (batch 1)
+    def weights(self, w, check=None):
+        """Device copy of [8112,10] host weights, re-uploaded only when their
+        values change (one compare per call; the serving engine keeps one
+        checkpoint for many requests, service.py:54-79).  `check` validates
+        and converts a new array (validation.check_weights); an array equal to
+        the cached one was validated already.  The device buffer's address
+        never changes, so captured graphs stay valid."""
+        torch = _torch()
+        if self._w_dev is None:
+            with torch.cuda.stream(self.stream):
+                self._w_dev = torch.empty((N_HIDDEN, N_OUTPUTS), dtype=torch.float64, device=self.device)
+        if self._w_host is not None and np.shape(w) == self._w_host.shape and np.array_equal(self._w_host, w):
+            return self._w_dev
+        host = check(w) if check is not None else np.asarray(w, dtype=np.float64)
+        if host.shape != (N_HIDDEN, N_OUTPUTS):
+            raise ValueError(f"expected weights of shape {(N_HIDDEN, N_OUTPUTS)}, got {host.shape}")
+        self._w_host = np.array(host, dtype=np.float64, copy=True)
+        with torch.cuda.stream(self.stream):
+            self._w_dev.copy_(torch.from_numpy(self._w_host).pin_memory(), non_blocking=True)
+        return self._w_dev
+
+    def infer_one(self, c, image: np.ndarray, w=None, check=None) -> np.ndarray:
+        """One presentation through a CUDA graph captured per configuration:
+        pinned H2D of the 784-byte image, one graph launch (k_prep ..
+        k_output), D2H of the counts.  Same kernels and results as infer().
+        Without `w`, the weights last set by weights() are used."""
+        torch = _torch()
+        d_w = self.weights(w, check) if w is not None else self._w_dev
+        key = bytes(c)
+        gr = self._graphs.get(key)
+        if gr is None:
+            ctab, _ = self.table(c)
+            with torch.cuda.stream(self.stream):
+                img_d = torch.zeros((1, N_INPUTS), dtype=torch.uint8, device=self.device)
+                cnt_d = torch.zeros((1, N_OUTPUTS), dtype=torch.int32, device=self.device)
+            ws_bytes = self.lib.snn_infer_workspace(ctypes.byref(c), 1)
+            with torch.cuda.stream(self.stream):
+                ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=self.device)
+            o = _native.InferOutC()
+            o.counts = cnt_d.data_ptr()
+            args = (ctypes.byref(c), img_d.data_ptr(), 1, d_w.data_ptr(), ctab.data_ptr(), ctypes.byref(o),
+                    ws.data_ptr(), ws_bytes, self.sptr)
+            _native.check(self.lib.snn_infer(*args))   # first launch: lazy attributes, module load
+            self.stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                _native.check(self.lib.snn_infer(*args))
+            gr = self._graphs[key] = {"g": g, "img": img_d, "cnt": cnt_d, "ws": ws, "c": c, "o": o,
+                                      "img_h": torch.zeros((1, N_INPUTS), dtype=torch.uint8).pin_memory(),
+                                      "cnt_h": torch.zeros((1, N_OUTPUTS), dtype=torch.int32).pin_memory()}
+        gr["img_h"].numpy()[0] = image.reshape(-1)
+        with torch.cuda.stream(self.stream):
+            gr["img"].copy_(gr["img_h"], non_blocking=True)
+            gr["g"].replay()
+            gr["cnt_h"].copy_(gr["cnt"], non_blocking=True)
+        self.stream.synchronize()
+        return gr["cnt_h"].numpy()[0].astype(np.int64)
 
     # ------------------------------------------------------------ training
     def train(self, c, images, labels, w):
