@@ -144,6 +144,11 @@ void snn_set_normad_cluster(int enable);
  * images of each snn_train call (NULL disables). */
 void snn_normad_phase_clocks(long long *d_clk);
 
+/* Profiling only -- results are WRONG while set: the cluster NormAD kernel
+ * skips phases (bit 0 output scan, 1 R adjoint, 2 dW, 3 G partials, 4 G
+ * gather) so their cost can be measured by difference.  0 = off (default). */
+void snn_normad_skip(int mask);
+
 /* Bytes of device workspace snn_train needs for n images. */
 size_t snn_train_workspace(const snn_consts_t *c, int64_t n_images);
 

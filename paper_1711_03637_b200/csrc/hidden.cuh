@@ -66,6 +66,8 @@ struct BatchArgs {
     uint16_t *tile_pos;      // [n][22][32] window of each lane, 0xFFFF = none
     int32_t *n_tiles;        // [n]
     int32_t *tile_base;      // [n+1] exclusive prefix of n_tiles
+    int32_t *n_win;          // [n]   active windows per image
+    int32_t *win_base;       // [n+1] exclusive prefix of n_win
     uint8_t *raster;         // sum(n_tiles) * nchunks * 512 spike-mask bytes (see raster_tc)
     int32_t items_per_tile;  // 1 (default bank) or 2 (generic bank)
     snn_infer_out_t out;     // counts / out_raster / ff / v_out / v_hid
@@ -145,19 +147,22 @@ __global__ void __launch_bounds__(kThreads) k_prep(const BatchArgs A) {
     for (int it = 0; it < kIters; ++it)
         if ((bal[it] >> lane) & 1u)
             tp[off[it] + __popc(bal[it] & ((1u << lane) - 1u))] = (uint16_t)(it * kThreads + tid);
-    if (tid == 0) A.n_tiles[img] = (run + kTile - 1) / kTile;
+    if (tid == 0) {
+        A.n_tiles[img] = (run + kTile - 1) / kTile;
+        A.n_win[img] = run;
+    }
 }
 
-// k_tile_scan: tile_base = exclusive prefix of n_tiles; one CTA, any n.
-__global__ void __launch_bounds__(1024) k_tile_scan(const BatchArgs A) {
-    __shared__ int s_w[32];
-    __shared__ int s_tot, s_carry;
+// k_tile_scan: tile_base / win_base = exclusive prefixes of n_tiles / n_win;
+// one CTA, any n.
+__device__ __forceinline__ void block_prefix(const int32_t *in, int32_t *out, int64_t n, int *s_w, int &s_tot,
+                                             int &s_carry) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_carry = 0;
     __syncthreads();
-    for (int64_t base = 0; base < A.n_images; base += 1024) {
+    for (int64_t base = 0; base < n; base += 1024) {
         const int64_t i = base + tid;
-        const int x = i < A.n_images ? A.n_tiles[i] : 0;
+        const int x = i < n ? in[i] : 0;
         int tot;
         const int ex = warp_excl_scan_int(x, &tot);
         if (lane == 0) s_w[warp] = tot;
@@ -169,12 +174,20 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const BatchArgs A) {
             if (lane == 0) s_tot = t2;
         }
         __syncthreads();
-        if (i < A.n_images) A.tile_base[i] = s_carry + s_w[warp] + ex;
+        if (i < n) out[i] = s_carry + s_w[warp] + ex;
         __syncthreads();
         if (tid == 0) s_carry += s_tot;
         __syncthreads();
     }
-    if (tid == 0) A.tile_base[A.n_images] = s_carry;
+    if (tid == 0) out[n] = s_carry;
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024) k_tile_scan(const BatchArgs A) {
+    __shared__ int s_w[32];
+    __shared__ int s_tot, s_carry;
+    block_prefix(A.n_tiles, A.tile_base, A.n_images, s_w, s_tot, s_carry);
+    block_prefix(A.n_win, A.win_base, A.n_images, s_w, s_tot, s_carry);
 }
 
 // ---------------------------------------------------------------------------
@@ -330,44 +343,53 @@ __device__ __forceinline__ unsigned hidden_step(const BatchArgs &A, const LifK &
     return m;
 }
 
-// k_hidden: persistent CTAs walk groups of kWPC consecutive work items.  With
-// the default bank (DEF) an item is a tile: a warp owns 32 windows x 12
-// features.  With a generic bank an item is (tile, half): 32 windows x 6
-// features, which keeps the 54 runtime taps of a warp within the register
-// budget.  The table chunks form one continuous stream across groups, so the
-// TMA ring never drains between groups.
-// One work item's lane state for the whole trial.
+// k_hidden work items: the active windows of the whole batch, image after
+// image, cut into groups of 32 (one per warp; with a generic bank an item is
+// a group and one half of the features, which keeps the 54 runtime taps of a
+// warp within the register budget).  A group may span two images: every lane
+// finds its own image and writes its masks into that image's raster block,
+// so no lane idles at image boundaries.
 struct ItemState {
     int64_t img;
-    int tile, pos, nt, half;
+    int pos, half;
     bool live, on;
     uint32_t lvp[3];  // the 9 pixel levels of this lane's window, 4 per word
     uint8_t *rout;    // this lane's raster bytes of chunk 0
-    size_t rstride;   // one chunk of this image
+    size_t rstride;   // one chunk of this lane's image
 };
+
+__device__ __forceinline__ int hidden_items(const BatchArgs &A, int ipt) {
+    return ipt * ((A.win_base[A.n_images] + kTile - 1) / kTile);
+}
 
 template <bool DEF>
 __device__ __forceinline__ void item_setup(const BatchArgs &A, int item, int total, int nchunks, ItemState &it) {
     const int lane = threadIdx.x & 31;
     const int64_t n = A.n_images;
     it.live = item < total;  // warp-uniform
-    const int gt = DEF ? item : item >> 1;
+    const int grp = DEF ? item : item >> 1;
     it.half = DEF ? 0 : item & 1;
+    const int gw = grp * kTile + lane;  // this lane's window in the batch
     it.img = 0;
-    it.tile = it.pos = it.nt = 0;
-    if (it.live) {
-        int64_t lo = 0, hi = n - 1;  // last image with tile_base <= gt
+    it.pos = 0xFFFF;
+    it.rout = nullptr;
+    it.rstride = 0;
+    if (it.live && gw < A.win_base[n]) {
+        int64_t lo = 0, hi = n - 1;  // last image with win_base <= gw
         while (lo < hi) {
             const int64_t mid = (lo + hi + 1) >> 1;
-            if (A.tile_base[mid] <= gt) lo = mid;
+            if (A.win_base[mid] <= gw) lo = mid;
             else hi = mid - 1;
         }
         it.img = lo;
-        it.tile = gt - A.tile_base[lo];
-        it.nt = A.n_tiles[lo];
-        it.pos = A.tile_pos[lo * (kMaxTiles * kTile) + it.tile * kTile + lane];
+        const int w = gw - A.win_base[lo];
+        const int nt = A.n_tiles[lo];
+        it.pos = A.tile_pos[lo * (kMaxTiles * kTile) + w];
+        it.rout = A.raster + raster_tc(A.tile_base[lo], nchunks, nt, 0, w / kTile) + it.half * (kRastTC / 2) +
+                  (w % kTile) * kChunk;
+        it.rstride = (size_t)nt * kRastTC;
     }
-    it.on = it.live && it.pos != 0xFFFF;
+    it.on = it.pos != 0xFFFF;
     const int p = it.on ? it.pos : 0;
     const int r = p / kFmap, col = p % kFmap;
     const uint8_t *im = A.images + it.img * (kSide * kSide);
@@ -380,10 +402,6 @@ __device__ __forceinline__ void item_setup(const BatchArgs &A, int item, int tot
             const uint32_t lev = it.on ? __ldg(im + (r + a) * kSide + col + b) : 0u;
             it.lvp[k >> 2] |= lev << (8 * (k & 3));
         }
-    it.rout = it.live ? A.raster + raster_tc(A.tile_base[it.img], nchunks, it.nt, 0, it.tile) +
-                            it.half * (kRastTC / 2) + lane * kChunk
-                      : nullptr;
-    it.rstride = (size_t)it.nt * kRastTC;
 }
 
 // The steps of one chunk for one live item (tab = the chunk's [8][256] table
@@ -416,9 +434,11 @@ __device__ __forceinline__ void item_chunk(const BatchArgs &A, const LifK &ph, c
         p0 |= (uint64_t)(m & 0x3Fu) << (8 * j);
         if (DEF) p1 |= (uint64_t)(m >> kHalf) << (8 * j);
     }
-    uint64_t *dst = reinterpret_cast<uint64_t *>(it.rout + (size_t)ch * it.rstride);
-    dst[0] = p0;
-    if (DEF) dst[kTile] = p1;  // the second half plane, 256 bytes on
+    if (it.on) {
+        uint64_t *dst = reinterpret_cast<uint64_t *>(it.rout + (size_t)ch * it.rstride);
+        dst[0] = p0;
+        if (DEF) dst[kTile] = p1;  // the second half plane, 256 bytes on
+    }
 }
 
 // Ring variant: the table streams through a 2-stage ring shared by the CTA's
@@ -431,8 +451,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
     const int N = A.c.n_steps;
     const int nchunks = (N + kChunk - 1) / kChunk;
     const int64_t n = A.n_images;
-    constexpr int kItemsPerTile = DEF ? 1 : 2;
-    const int total = kItemsPerTile * A.tile_base[n];
+    const int total = hidden_items(A, DEF ? 1 : 2);
     const int ngroups = (total + kWPC - 1) / kWPC;
     if ((int)blockIdx.x >= ngroups) return;
     const int my_groups = (ngroups - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
@@ -491,8 +510,7 @@ __global__ void __launch_bounds__(kResWarps * 32, 1) k_hidden_res(const BatchArg
     const int N = A.c.n_steps;
     const int nchunks = (N + kChunk - 1) / kChunk;
     const int64_t n = A.n_images;
-    constexpr int kItemsPerTile = DEF ? 1 : 2;
-    const int total = kItemsPerTile * A.tile_base[n];
+    const int total = hidden_items(A, DEF ? 1 : 2);
     if (tid == 0) {
         mbar_init(&r_full, 1);
         fence_mbar_init();
@@ -692,6 +710,7 @@ __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double
     const uint8_t *b0 = reinterpret_cast<const uint8_t *>(S.pl[0]) + jl, *b1 = reinterpret_cast<const uint8_t *>(S.pl[1]) + jl;
     for (int t = 0; t < nt; ++t) {
         __syncwarp();
+        if (S.pos[t * kTile + lane] == 0xFFFF) n0 = n1 = 0ull;  // raster bytes exist only for windows
         S.pl[0][lane] = n0;
         S.pl[1][lane] = n1;
         const bool any = __any_sync(kFull, (n0 | n1) != 0ull);
@@ -775,8 +794,10 @@ __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double
         double g = 0.0;
         for (int t = 0; t < nt; ++t) {
             const uint8_t *src = R + (size_t)t * kRastTC;
-            unsigned m = chunk_mask(__ldcs(reinterpret_cast<const unsigned long long *>(src)),
-                                    __ldcs(reinterpret_cast<const unsigned long long *>(src + kRastTC / 2)), j);
+            unsigned m = S.pos[t * kTile + lane] == 0xFFFF
+                             ? 0u
+                             : chunk_mask(__ldcs(reinterpret_cast<const unsigned long long *>(src)),
+                                          __ldcs(reinterpret_cast<const unsigned long long *>(src + kRastTC / 2)), j);
             int tt;
             int k = warp_excl_scan_int(__popc(m), &tt);
             const int id0 = (int)S.pos[t * kTile + lane] * kNF;

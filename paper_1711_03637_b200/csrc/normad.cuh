@@ -35,6 +35,8 @@ struct TrainWS {
     uint16_t *tile_pos; // [n][22][32]
     int32_t *n_tiles;   // [n]
     int32_t *tile_base; // [n+1]
+    int32_t *n_win;     // [n]   active windows per image
+    int32_t *win_base;  // [n+1]
     int32_t *n_act;     // [n]
     uint16_t *act_k;    // [n][8112]  active neuron ids, ascending
     int32_t *act_off;   // [n][8113]  per active neuron: start in nsp

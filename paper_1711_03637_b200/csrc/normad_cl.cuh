@@ -68,6 +68,7 @@ struct ShardWS {
     uint16_t *snsp;   // [n][evcap]        shard-major spike steps of the active neurons
     double *undo;     // [kCl][kClRows][10] old rows of the last committed image
     int push;         // partials / R pushed through DSMEM stores (normad_cl_smem_bytes)
+    int skip;         // profiling only (snn_normad_skip): bit 0 scan, 1 R, 2 dW, 3 G partials, 4 gather
 };
 
 // one image's lists of one shard, staged (or pointing into global memory
@@ -338,7 +339,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
         stamp(0);
         const ClBuf &B = s_buf[i & 1];
         // ---- G partials of this shard (ascending id within the shard)
-        for (int t = tid; t < N * kNO; t += kClThreads) {
+        for (int t = tid; t < ((SW.skip & 8) ? 0 : N * kNO); t += kClThreads) {
             const int s = t / kNO, l = t - s * kNO;
             const int e1 = B.soff[s + 1];
             double g = 0.0;
@@ -377,7 +378,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
         const bool more = i + 1 < T.n;
         if (r == 0) {
             // G = P_0 + P_1 + ... + P_{kCl-1}, in rank order
-            for (int t = tid; t < N * kNO; t += kClThreads) {
+            for (int t = tid; t < ((SW.skip & 16) ? 0 : N * kNO); t += kClThreads) {
                 double v[kCl];
 #pragma unroll
                 for (int q = 0; q < kCl; ++q)
@@ -395,7 +396,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
                 const int l = lane < kNO ? lane : kNO - 1;
                 OutState st;
                 out_init(st, c);
-                for (int s = 0; s < N; ++s) {
+                for (int s = 0; s < ((SW.skip & 1) ? 0 : N); ++s) {
                     double ff;
                     out_step(st, c, P[s * kNO + l], s, l, &ff);
                     if (lane == 0) OMASK[s] = (uint16_t)st.prev;
@@ -425,7 +426,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
             // R(u, l) = sum_{s >= u} sigma(s, l) H(s - u): adjoint of kernel -> d_hat, backward
             if (warp == 0 && lane < kNO) {
                 double pd = 0.0, pa = 0.0, pb = 0.0;
-                for (int u = N - 1; u >= 0; --u) {
+                for (int u = (SW.skip & 2) ? -1 : N - 1; u >= 0; --u) {
                     pd = __dadd_rn(__dmul_rn(pd, c.decay_learn), SR[u * kNO + lane]);
                     const double q = __dmul_rn(pd, c.dhat_scale);
                     pa = __dadd_rn(__dmul_rn(pa, c.decay_slow), q);
@@ -452,7 +453,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
         stamp(8);
         // dW for the shard's active neurons (spikes ascending); commit with an undo log
         bool bad = false;
-        for (int a = tid; a < B.n_act; a += kClThreads) {
+        for (int a = tid; a < ((SW.skip & 4) ? 0 : B.n_act); a += kClThreads) {
             const int row = B.act[a];
             double acc[kNO];
 #pragma unroll

@@ -60,7 +60,7 @@ size_t raster_bytes(const snn_consts_t *c, int64_t n) { return (size_t)n * kMaxT
 // ---- inference workspace: tile_pos | n_tiles | tile_base | raster (upper bound)
 struct InferWS {
     uint16_t *tile_pos;
-    int32_t *n_tiles, *tile_base;
+    int32_t *n_tiles, *tile_base, *n_win, *win_base;
     uint8_t *raster;
     double *g;  // [n][N][10] G rows (k_gsum -> k_output)
 };
@@ -76,6 +76,8 @@ size_t infer_ws_layout(const snn_consts_t *c, int64_t n, char *base, InferWS *w)
     x.tile_pos = (uint16_t *)take((size_t)n * kMaxTiles * kTile * 2);
     x.n_tiles = (int32_t *)take((size_t)n * 4);
     x.tile_base = (int32_t *)take((size_t)(n + 1 + kMaxSub) * 4);
+    x.n_win = (int32_t *)take((size_t)n * 4);
+    x.win_base = (int32_t *)take((size_t)(n + 1 + kMaxSub) * 4);
     x.raster = (uint8_t *)take(raster_bytes(c, n));
     x.g = (double *)take((size_t)n * c->n_steps * kNO * 8);
 
@@ -96,7 +98,7 @@ int64_t train_evcap(const snn_consts_t *c) {
 size_t train_ws_per_image(const snn_consts_t *c) {
     const size_t N = c->n_steps, cap = train_evcap(c);
     return raster_bytes(c, 1) + kMaxTiles * kTile * 2 + 4 + 4 + 4 + kNH * 2 + (kNH + 1) * 4 + cap * 2 +
-           (N + 1) * 4 + cap * 2 + N * 8 + kMaxTiles * N * 8 + 3 * (kCl + 1) * 4 + kCl * (N + 1) * 4 + 2 * cap * 2 +
+           (N + 1) * 4 + cap * 2 + N * 8 + kMaxTiles * N * 8 + 3 * (kCl + 1) * 4 + 8 + kCl * (N + 1) * 4 + 2 * cap * 2 +
            N * 8 + kNH * 2 * 2 + (kNH + kCl) * 4 + (size_t)kCl * kClRows * kNO * 8 / 64;
 }
 
@@ -120,6 +122,8 @@ size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base, 
     w.tile_pos = (uint16_t *)take(n * kMaxTiles * kTile * 2);
     w.n_tiles = (int32_t *)take(n * 4);
     w.tile_base = (int32_t *)take((n + 1) * 4);
+    w.n_win = (int32_t *)take(n * 4);
+    w.win_base = (int32_t *)take((n + 1) * 4);
     w.n_act = (int32_t *)take(n * 4);
     w.act_k = (uint16_t *)take(n * kNH * 2);
     w.act_off = (int32_t *)take(n * (kNH + 1) * 4);
@@ -165,6 +169,7 @@ int g_hid_ctas = 0;
 int g_hid_res = 1;  // snn_set_hidden_resident
 int g_normad_cluster = 1;  // snn_set_normad_cluster
 long long *g_phase_clk = nullptr;  // snn_normad_phase_clocks
+int g_normad_skip = 0;             // snn_normad_skip (profiling only)
 int64_t g_pipe_images = 0;
 
 // prep -> tile scan -> hidden (persistent): the hidden raster of A's images
@@ -320,6 +325,8 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
     A.tile_pos = out->tile_pos ? out->tile_pos : w.tile_pos;
     A.n_tiles = out->n_tiles ? out->n_tiles : w.n_tiles;
     A.tile_base = out->tile_base ? out->tile_base : w.tile_base;
+    A.n_win = w.n_win;
+    A.win_base = w.win_base;
     A.raster = out->raster ? out->raster : w.raster;
 
     A.out = *out;
@@ -345,6 +352,8 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
         B.tile_pos = w.tile_pos + i0 * kMaxTiles * kTile;
         B.n_tiles = w.n_tiles + i0;
         B.tile_base = w.tile_base + i0 + b;
+        B.n_win = w.n_win + i0;
+        B.win_base = w.win_base + i0 + b;
         B.raster = w.raster + (size_t)i0 * kMaxTiles * nch * kRastTC;
         B.out.counts = out->counts + i0 * kNO;
         if (out->out_raster) B.out.out_raster = out->out_raster + i0 * N;
@@ -365,6 +374,8 @@ extern "C" void snn_set_normad_cluster(int enable) { g_normad_cluster = enable; 
 extern "C" void snn_set_hidden_resident(int enable) { g_hid_res = enable; }
 
 extern "C" void snn_normad_phase_clocks(long long *d_clk) { g_phase_clk = d_clk; }
+
+extern "C" void snn_normad_skip(int mask) { g_normad_skip = mask; }
 
 extern "C" void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_per_sm) {
     g_pipe_images = images_per_subbatch;
@@ -403,6 +414,7 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     const size_t need = train_ws(c, chunk, &T.ws, (char *)d_ws, &SW);
     SW.clk = g_phase_clk;
     SW.push = cl_push ? 1 : 0;
+    SW.skip = g_normad_skip;
     if (!d_ws || ws_bytes < need) return set_error(SNN_ENOMEM, "workspace too small");
     if (use_cl) {
         if (cudaFuncSetAttribute(k_normad_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem) != cudaSuccess)
@@ -426,6 +438,8 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
         A.tile_pos = T.ws.tile_pos;
         A.n_tiles = T.ws.n_tiles;
         A.tile_base = T.ws.tile_base;
+        A.n_win = T.ws.n_win;
+        A.win_base = T.ws.win_base;
         A.items_per_tile = is_default_bank(*c) ? 1 : 2;
         if ((rc = is_default_bank(*c) ? launch_fast<true>(A, nullptr, s) : launch_fast<false>(A, nullptr, s)))
             return rc;
