@@ -141,12 +141,15 @@ void snn_set_normad_cluster(int enable);
 
 /* Profiling hook: when d_clk (device, int64 [64][16]) is set, the cluster
  * NormAD kernel records clock64() at its phase boundaries for the first 64
- * images of each snn_train call (NULL disables). */
+ * images of each snn_train call (NULL disables).  Effective only in the
+ * profiling build (-DSNN_NORMAD_PROFILE, build.py --profile); a no-op in the
+ * product library. */
 void snn_normad_phase_clocks(long long *d_clk);
 
 /* Profiling only -- results are WRONG while set: the cluster NormAD kernel
  * skips phases (bit 0 output scan, 1 R adjoint, 2 dW, 3 G partials, 4 G
- * gather) so their cost can be measured by difference.  0 = off (default). */
+ * gather) so their cost can be measured by difference.  0 = off (default).
+ * Effective only in the profiling build, like snn_normad_phase_clocks. */
 void snn_normad_skip(int mask);
 
 /* Bytes of device workspace snn_train needs for n images. */

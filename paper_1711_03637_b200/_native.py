@@ -11,6 +11,7 @@ import os
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsnn_b200.so")
 
+
 SNN_OK = 0
 SNN_ENOMEM = 12
 SNN_EINVAL = 22
@@ -87,11 +88,13 @@ def load():
     global _LIB
     if _LIB is not None:
         return _LIB
-    if not os.path.exists(LIB_PATH):
+    # profiling scripts only: an alternative in-tree build (build.py --profile)
+    path = os.environ.get("SNN_B200_LIB", LIB_PATH)
+    if not os.path.exists(path):
         raise ImportError(
-            f"{LIB_PATH} is missing: the CUDA extension has not been built "
+            f"{path} is missing: the CUDA extension has not been built "
             "(python -m paper_1711_03637_b200.build). There is no CPU fallback.")
-    lib = ctypes.CDLL(LIB_PATH)
+    lib = ctypes.CDLL(path)
     for name, res, args in SIGNATURES:
         fn = getattr(lib, name)
         fn.restype = res

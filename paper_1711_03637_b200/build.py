@@ -58,5 +58,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+PROFILE_OUT = os.path.join(HERE, "libsnn_b200_profile.so")
+
+
+def build_profile(force: bool = False) -> str:
+    """Profiling-only build (-DSNN_NORMAD_PROFILE): the cluster NormAD kernel
+    with phase clocks and phase ablation compiled in.  Never loaded by the
+    product path; scripts select it with SNN_B200_LIB (see _native.py)."""
+    if force or not os.path.exists(PROFILE_OUT) or any(os.path.getmtime(d) > os.path.getmtime(PROFILE_OUT) for d in DEPS):
+        subprocess.run([nvcc(), *NVCC_FLAGS, "-DSNN_NORMAD_PROFILE", "-I", os.path.join(ROOT, "include"),
+                        "-o", PROFILE_OUT, SRC], check=True)
+    return PROFILE_OUT
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--profile" in sys.argv:
+        print(build_profile(force="--force" in sys.argv))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

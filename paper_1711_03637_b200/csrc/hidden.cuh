@@ -450,7 +450,6 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
     const int tid = threadIdx.x, warp = tid >> 5;
     const int N = A.c.n_steps;
     const int nchunks = (N + kChunk - 1) / kChunk;
-    const int64_t n = A.n_images;
     const int total = hidden_items(A, DEF ? 1 : 2);
     const int ngroups = (total + kWPC - 1) / kWPC;
     if ((int)blockIdx.x >= ngroups) return;
@@ -509,7 +508,6 @@ __global__ void __launch_bounds__(kResWarps * 32, 1) k_hidden_res(const BatchArg
     const int tid = threadIdx.x, warp = tid >> 5;
     const int N = A.c.n_steps;
     const int nchunks = (N + kChunk - 1) / kChunk;
-    const int64_t n = A.n_images;
     const int total = hidden_items(A, DEF ? 1 : 2);
     if (tid == 0) {
         mbar_init(&r_full, 1);

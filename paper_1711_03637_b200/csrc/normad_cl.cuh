@@ -330,16 +330,27 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
     cluster.sync();
 
     bool failed = false;
+    // profiling builds only (-DSNN_NORMAD_PROFILE): phase clocks and phase
+    // ablation.  The product kernel compiles neither: even dead hooks change
+    // the register allocation of the serial output scan.
+#ifdef SNN_NORMAD_PROFILE
+    const int skip = SW.skip;
     long long *clk = nullptr;
     auto stamp = [&](int ph) {
         if (clk && tid == 0) clk[ph] = clock64();
     };
+#else
+    constexpr int skip = 0;
+    auto stamp = [](int) {};
+#endif
     for (int64_t i = 0; i < T.n; ++i) {
+#ifdef SNN_NORMAD_PROFILE
         clk = (SW.clk && r == 0 && T.first + i < 64) ? SW.clk + (T.first + i) * 16 : nullptr;
+#endif
         stamp(0);
         const ClBuf &B = s_buf[i & 1];
         // ---- G partials of this shard (ascending id within the shard)
-        for (int t = tid; t < ((SW.skip & 8) ? 0 : N * kNO); t += kClThreads) {
+        for (int t = tid; t < ((skip & 8) ? 0 : N * kNO); t += kClThreads) {
             const int s = t / kNO, l = t - s * kNO;
             const int e1 = B.soff[s + 1];
             double g = 0.0;
@@ -378,7 +389,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
         const bool more = i + 1 < T.n;
         if (r == 0) {
             // G = P_0 + P_1 + ... + P_{kCl-1}, in rank order
-            for (int t = tid; t < ((SW.skip & 16) ? 0 : N * kNO); t += kClThreads) {
+            for (int t = tid; t < ((skip & 16) ? 0 : N * kNO); t += kClThreads) {
                 double v[kCl];
 #pragma unroll
                 for (int q = 0; q < kCl; ++q)
@@ -396,14 +407,23 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
                 const int l = lane < kNO ? lane : kNO - 1;
                 OutState st;
                 out_init(st, c);
-                for (int s = 0; s < ((SW.skip & 1) ? 0 : N); ++s) {
+                const double *gp = P + l;
+                uint16_t *om = OMASK;
+                const int ns = (skip & 1) ? 0 : N;
+                for (int s = 0; s < ns; ++s) {
                     double ff;
-                    out_step(st, c, P[s * kNO + l], s, l, &ff);
-                    if (lane == 0) OMASK[s] = (uint16_t)st.prev;
+                    out_step(st, c, gp[s * kNO], s, l, &ff);
+                    if (lane == 0) om[s] = (uint16_t)st.prev;
                 }
                 if (lane < kNO) T.counts[(size_t)i * kNO + lane] = st.cnt;
+#ifdef SNN_NORMAD_PROFILE
+                if (clk && lane == 0) clk[12] = clock64();
+#endif
             } else if (more) {
                 stage(i + 1, (int)((i + 1) & 1), 32, kClThreads - 32);
+#ifdef SNN_NORMAD_PROFILE
+                if (clk && lane == 0) atomicMax((unsigned long long *)&clk[13], (unsigned long long)clock64());
+#endif
             }
             __syncthreads();
             stamp(4);
@@ -426,7 +446,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
             // R(u, l) = sum_{s >= u} sigma(s, l) H(s - u): adjoint of kernel -> d_hat, backward
             if (warp == 0 && lane < kNO) {
                 double pd = 0.0, pa = 0.0, pb = 0.0;
-                for (int u = (SW.skip & 2) ? -1 : N - 1; u >= 0; --u) {
+                for (int u = (skip & 2) ? -1 : N - 1; u >= 0; --u) {
                     pd = __dadd_rn(__dmul_rn(pd, c.decay_learn), SR[u * kNO + lane]);
                     const double q = __dmul_rn(pd, c.dhat_scale);
                     pa = __dadd_rn(__dmul_rn(pa, c.decay_slow), q);
@@ -453,7 +473,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
         stamp(8);
         // dW for the shard's active neurons (spikes ascending); commit with an undo log
         bool bad = false;
-        for (int a = tid; a < ((SW.skip & 4) ? 0 : B.n_act); a += kClThreads) {
+        for (int a = tid; a < ((skip & 4) ? 0 : B.n_act); a += kClThreads) {
             const int row = B.act[a];
             double acc[kNO];
 #pragma unroll

@@ -1,10 +1,14 @@
 """Cost of each phase of the cluster NormAD kernel by ablation (snn_normad_skip;
-results are wrong while a phase is skipped -- timing only)."""
+results are wrong while a phase is skipped -- timing only).  Runs the profiling
+build (build.py --profile), whose serial scan compiles differently from the
+product kernel: absolute times are higher than bench.py's, differences indicative."""
 import os, sys
 import numpy as np
 import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+from paper_1711_03637_b200 import build as _build  # noqa: E402
+os.environ["SNN_B200_LIB"] = _build.build_profile()  # hooks are compiled only into the profile build
 import paper_1711_03637_b200 as sd  # noqa: E402
 from paper_1711_03637_b200.engine import get_engine, make_consts  # noqa: E402
 d = np.load(os.path.join(ROOT, "data", "workloads.npz"))

@@ -8,6 +8,8 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+from paper_1711_03637_b200 import build as _build  # noqa: E402
+os.environ["SNN_B200_LIB"] = _build.build_profile()  # hooks are compiled only into the profile build
 import paper_1711_03637_b200 as sd  # noqa: E402
 from paper_1711_03637_b200.engine import get_engine, make_consts  # noqa: E402
 
@@ -32,6 +34,7 @@ print("cycles per phase (median over images 4..63):")
 for i, n in enumerate(names[:11]):
     print(f"  {n:12s} {np.median(d_[:, i]):8.0f}")
 print(f"  {'to next img':12s} {np.median(nxt):8.0f}")
-print("scan cycles per image:", d_[:, 3].tolist())
+print("scan cycles per image:", d_[:, 3].tolist()[:8])
+print("scan warp loop (median):", np.median(k[:, 12] - k[:, 3]), " stage warps (median):", np.median(k[:, 13] - k[:, 3]))
 tot = np.median(k[1:, 0] - k[:-1, 0])
 print(f"  per image    {tot:8.0f} cycles = {tot / 1.965e3:.2f} us at 1965 MHz")
