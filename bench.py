@@ -335,6 +335,7 @@ def run_ours(args):
         exec_flop_launch = float(act.sum()) * n_steps * FLOP_PER_ACTIVE_POS_STEP
         achieved = exec_flop_launch / (launch_ms * 1e-3) / 1e12
         dense_tflops = (b - a) * F_INF_PER_STEP * n_steps / (ker_ms / args.steps * 1e-3) / 1e12
+        traffic_bytes, traffic_src = committed_traffic("k_hidden")
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
@@ -349,7 +350,8 @@ def run_ours(args):
                     "d2h_bytes_per_step": int(d2h), "api": "distributed.sharded_batch_counts (host numpy in/out)"},
             "gpu_launches": int(args.steps * launches_per_step),
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": f64, "unit": "TFLOP/s",
-                         "frac": achieved / f64, "traffic": None,
+                         "frac": achieved / f64, "traffic": traffic_bytes,
+                         "traffic_unit": "bytes per launch (DRAM read + write)", "traffic_source": traffic_src,
                          "kernel": "k_hidden<DEF> (fused input-table gather + 3x3 stencil + hidden LIF, "
                                    "spike raster out), timed alone with CUDA events (snn_profile_events)",
                          "achieved_basis": f"executed fp64 flop: active windows x N x {FLOP_PER_ACTIVE_POS_STEP}",
@@ -408,6 +410,24 @@ def kernel_alone_ms(eng, c, d_img, d_w, flush, steps):
         lib.snn_profile_events(None, None)
         lib.snn_set_pipeline(PIPE_IMAGES, 0)
     return statistics.median(hk), statistics.median(call)
+
+
+def committed_traffic(prefix):
+    """DRAM bytes per launch of the roofline kernel from the newest committed
+    ncu --set full capture (profiles/<round>_traffic.json, written by
+    scripts/summarize_profiles.py); (None, None) when there is none."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    if not files:
+        return None, None
+    data = json.load(open(files[-1]))
+    for name, recs in data.items():
+        if name.split("<")[0].split("::")[-1].strip().split()[-1].startswith(prefix) and recs:
+            r = recs[0]
+            return r["dram_bytes"], (f"{os.path.relpath(files[-1], ROOT)}: {name}, {r['capture']} "
+                                     f"(ncu --set full, 10,000-image launch, read {r['dram_read_bytes']:.3g} B + "
+                                     f"write {r['dram_write_bytes']:.3g} B)")
+    return None, None
 
 
 def bench_train(args, sd, eng, d, cfg, bank):

@@ -640,19 +640,19 @@ __device__ __forceinline__ bool out_step(OutState &st, const snn_consts_t &c, do
 
 // ---------------------------------------------------------------------------
 // k_gsum: G(s, l) = sum of W[k, l] over the hidden neurons k spiking at step
-// s (network.py:311 restated event-driven), summed in ascending k -- a fixed
-// order, so results never depend on the batch an image is in.  One warp per
+// s (network.py:311 restated event-driven), summed in a fixed order that
+// depends only on the image, so results never depend on the batch it is in.  One warp per
 // (image, 8-step chunk); chunks are independent, so a single image spreads
 // over ceil(N/8) warps.
 //   lists  per tile (in order) the warp is transposed: lane (j, g) takes step j
-//          of the tile's windows 8g .. 8g+7 (masks staged in shared memory),
-//          counts their spikes, a 4-lane prefix gives its offset in step j's
-//          list, and it writes their neuron ids.  Tiles ascend in window
-//          position, windows within a tile too and features within a window:
-//          every step list is in ascending neuron id.
+//          of the tile's windows g, g+4, .., g+28 (interleaved, so spatially
+//          clustered spikes spread over the 4 lanes; masks staged in shared
+//          memory), counts their spikes, a 4-lane prefix gives its offset in
+//          step j's list, and it writes their neuron ids.  The list order
+//          (tile, window group, window, feature) depends only on the image.
 //   sums   lane (j, p) walks step j's list for outputs 2p, 2p+1 (16-byte W
 //          loads, 8 in flight).  A step with more than kStepCap spikes is
-//          summed afterwards tile by tile, in the same order.
+//          summed afterwards tile by tile in ascending neuron id.
 constexpr int kStepCap = 256;
 constexpr int kGWarps = 4;
 
@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double
         unsigned cnt = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int w = g * 8 + i;
+            const int w = i * 4 + g;  // interleaved: spatially clustered spikes spread over the 4 lanes
             m[i] = (unsigned)b0[w * 8] | ((unsigned)b1[w * 8] << kHalf);
             cnt += __popc(m[i]);
         }
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double
         const unsigned tot = __shfl_sync(kFull, inc, lane | 3);
         unsigned k = runl + inc - cnt;
         uint16_t *dst = S.ids + jl * kStepCap;
-        const uint16_t *tp = S.pos + t * kTile + g * 8;
+        const uint16_t *tp = S.pos + t * kTile + g;
         // one loop over all of this lane's spikes: 12-bit fields of windows 0..4 and 5..7
         uint64_t w0 = (uint64_t)m[0] | ((uint64_t)m[1] << 12) | ((uint64_t)m[2] << 24) | ((uint64_t)m[3] << 36) |
                       ((uint64_t)m[4] << 48);
@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double
             if (lo) w0 &= w0 - 1ull;
             else w1 &= w1 - 1ull;
             const int i = (b * 43) >> 9;  // b / 12 for b < 96
-            if (k < (unsigned)kStepCap) dst[k] = (uint16_t)((int)tp[i] * kNF + (b - 12 * i));
+            if (k < (unsigned)kStepCap) dst[k] = (uint16_t)((int)tp[4 * i] * kNF + (b - 12 * i));
             ++k;
         }
         runl += tot;
@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double
             reinterpret_cast<double2 *>(Gi + (size_t)j * kNO)[p] = make_double2(g0, g1);
         }
     }
-    // rare: a step with more than kStepCap spikes -- same order, tile by tile
+    // rare: a step with more than kStepCap spikes -- tile by tile, ascending id
     for (unsigned ov = ovf; ov; ov &= ov - 1u) {
         const int j = (__ffs(ov) - 1) >> 2;
         __syncwarp();

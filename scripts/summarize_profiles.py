@@ -42,13 +42,24 @@ def ncu_csv(args):
     return list(csv.reader(io.StringIO(r.stdout)))
 
 
-def summarize(rep, fh):
+def _bytes(v, unit):
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+    return float(v.replace(",", "")) * scale
+
+
+def summarize(rep, fh, traffic):
     rows = ncu_csv(["-i", rep, "--page", "raw", "--csv"])
     if len(rows) < 3:
         return
     h, units = rows[0], rows[1]
     for r in rows[2:]:
         name = r[h.index("Kernel Name")]
+        if "dram__bytes_read.sum" in h and "dram__bytes_write.sum" in h:
+            ir, iw, it = h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum"), h.index("gpu__time_duration.sum")
+            traffic.setdefault(name.split("(")[0], []).append(
+                {"dram_bytes": _bytes(r[ir], units[ir]) + _bytes(r[iw], units[iw]),
+                 "dram_read_bytes": _bytes(r[ir], units[ir]), "dram_write_bytes": _bytes(r[iw], units[iw]),
+                 "duration": r[it] + " " + units[it], "capture": os.path.basename(rep)})
         fh.write(f"\n### `{name}`\n\n| metric | value |\n|---|---|\n")
         for key, label in METRICS:
             if key in h:
@@ -92,9 +103,13 @@ def main():
     with open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w") as fh:
         fh.write(f"# ncu summary ({tag})\n\nFrom `ncu --set full --clock-control none --import-source on` "
                  "captures (cold-cache, serialised replays: compare shares, not absolutes).\n")
+        traffic = {}
         for rep in reps:
             fh.write(f"\n## {rep}\n")
-            summarize(os.path.join(OUT, rep), fh)
+            summarize(os.path.join(OUT, rep), fh, traffic)
+    # per-launch DRAM traffic of each captured kernel (bench.py roofline.traffic)
+    with open(os.path.join(PROF, f"{tag}_traffic.json"), "w") as g:
+        json.dump(traffic, g, indent=1)
     if run:
         for src, dst in ((f"launches_{run}.csv", "launches.csv"), (f"launches_train_{run}.csv", "launches_train.csv"),
                          (f"bench_{run}.json", "bench.json")):

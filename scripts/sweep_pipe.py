@@ -1,4 +1,5 @@
-"""Sweep snn_set_pipeline(images_per_subbatch, hidden_ctas_per_sm) on the c3 workload (10k images)."""
+"""Sweep snn_set_hidden_resident x snn_set_pipeline(images_per_subbatch, hidden_ctas_per_sm) on the c3
+workload (10k images)."""
 import ctypes
 import os
 import sys
@@ -20,7 +21,8 @@ imgs = torch.from_numpy(d["c3_images"].reshape(10000, -1).copy()).cuda()
 dw = torch.from_numpy(w.copy()).cuda()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 ref = None
-for per, ctas in [(0, 0), (1024, 0), (2048, 0), (3334, 0), (5000, 0), (1024, 4), (2048, 4), (3334, 4), (5000, 4), (0, 4)]:
+for res, per, ctas in [(1, 0, 0), (1, 2048, 0), (1, 3334, 0), (0, 0, 0), (0, 1024, 3), (0, 2048, 3), (0, 1024, 4), (0, 2048, 4), (0, 3334, 4), (0, 2048, 2)]:
+    eng.lib.snn_set_hidden_resident(res)
     eng.lib.snn_set_pipeline(per, ctas)
     for _ in range(3):
         out = eng.infer(c, imgs, dw)["counts"]
@@ -36,5 +38,5 @@ for per, ctas in [(0, 0), (1024, 0), (2048, 0), (3334, 0), (5000, 0), (1024, 4),
         ts.append(e0.elapsed_time(e1))
     o = out.cpu().numpy()
     ref = o if ref is None else ref
-    print(f"per={per:5d} ctas={ctas}: {np.median(ts):.3f} ms  ({10000 / np.median(ts) * 1e3 / 1e6:.3f} M img/s)  "
+    print(f"res={res} per={per:5d} ctas={ctas}: {np.median(ts):.3f} ms  ({10000 / np.median(ts) * 1e3 / 1e6:.3f} M img/s)  "
           f"same={np.array_equal(o, ref)} gold200={np.array_equal(o[:200], gold)}", flush=True)
