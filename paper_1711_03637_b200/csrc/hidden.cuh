@@ -677,24 +677,24 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t x) {
     return x;
 }
 
+template <int CAP>
 struct GsumSmem {
-    uint16_t ids[kChunk * kStepCap];  // the chunk's step lists
+    uint16_t ids[kChunk * CAP];       // the chunk's step lists
     uint16_t pos[kMaxTiles * kTile];  // window position of each (tile, lane)
     uint64_t pl[2][kTile];            // the current tile's two mask planes, per window
 };
 
-__global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double *G) {
-    __shared__ __align__(16) GsumSmem smem[kGWarps];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    GsumSmem &S = smem[warp];
+// One (image, chunk) task of one warp: lists, then sums, into G's chunk rows.
+template <int CAP>
+__device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, int64_t img, int ch, GsumSmem<CAP> &S) {
+    const int kStepCap = CAP;
+    const int lane = threadIdx.x & 31;
     const int N = A.c.n_steps, nch = n_chunks(N);
-    const int64_t task = (int64_t)blockIdx.x * kGWarps + warp;
-    if (task >= A.n_images * nch) return;
-    const int64_t img = task / nch;
-    const int ch = (int)(task - img * nch);
     const int s0 = ch * kChunk, ns = min(kChunk, N - s0);
+    __syncwarp();  // a warp running several tasks: the previous one is done with S
     const int nt = A.n_tiles[img];
     for (int k = lane; k < nt * kTile; k += 32) S.pos[k] = A.tile_pos[img * (kMaxTiles * kTile) + k];
+    const uint16_t *PP = S.pos;
     const uint8_t *R = A.raster + raster_tc(A.tile_base[img], nch, nt, ch, 0) + lane * kChunk;
     const double *W = A.w;
     // ---- lists: lane (jl, g) = (step, window group of 8)
@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double
     const uint8_t *b0 = reinterpret_cast<const uint8_t *>(S.pl[0]) + jl, *b1 = reinterpret_cast<const uint8_t *>(S.pl[1]) + jl;
     for (int t = 0; t < nt; ++t) {
         __syncwarp();
-        if (S.pos[t * kTile + lane] == 0xFFFF) n0 = n1 = 0ull;  // raster bytes exist only for windows
+        if (PP[t * kTile + lane] == 0xFFFF) n0 = n1 = 0ull;  // raster bytes exist only for windows
         S.pl[0][lane] = n0;
         S.pl[1][lane] = n1;
         const bool any = __any_sync(kFull, (n0 | n1) != 0ull);
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double
         const unsigned tot = __shfl_sync(kFull, inc, lane | 3);
         unsigned k = runl + inc - cnt;
         uint16_t *dst = S.ids + jl * kStepCap;
-        const uint16_t *tp = S.pos + t * kTile + g;
+        const uint16_t *tp = PP + t * kTile + g;
         // one loop over all of this lane's spikes: 12-bit fields of windows 0..4 and 5..7
         uint64_t w0 = (uint64_t)m[0] | ((uint64_t)m[1] << 12) | ((uint64_t)m[2] << 24) | ((uint64_t)m[3] << 36) |
                       ((uint64_t)m[4] << 48);
@@ -792,13 +792,13 @@ __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double
         double g = 0.0;
         for (int t = 0; t < nt; ++t) {
             const uint8_t *src = R + (size_t)t * kRastTC;
-            unsigned m = S.pos[t * kTile + lane] == 0xFFFF
+            unsigned m = PP[t * kTile + lane] == 0xFFFF
                              ? 0u
                              : chunk_mask(__ldcs(reinterpret_cast<const unsigned long long *>(src)),
                                           __ldcs(reinterpret_cast<const unsigned long long *>(src + kRastTC / 2)), j);
             int tt;
             int k = warp_excl_scan_int(__popc(m), &tt);
-            const int id0 = (int)S.pos[t * kTile + lane] * kNF;
+            const int id0 = (int)PP[t * kTile + lane] * kNF;
             while (m) {
                 const int f = __ffs(m) - 1;
                 m &= m - 1u;
@@ -811,6 +811,16 @@ __global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double
         }
         if (lane < kNO) Gi[(size_t)j * kNO + lane] = g;
     }
+}
+
+__global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double *G) {
+    __shared__ __align__(16) GsumSmem<kStepCap> smem[kGWarps];
+    const int warp = threadIdx.x >> 5;
+    const int nch = n_chunks(A.c.n_steps);
+    const int64_t task = (int64_t)blockIdx.x * kGWarps + warp;
+    if (task >= A.n_images * nch) return;
+    const int64_t img = task / nch;
+    gsum_task<kStepCap>(A, G, img, (int)(task - img * nch), smem[warp]);
 }
 
 // ---------------------------------------------------------------------------
