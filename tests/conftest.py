@@ -47,3 +47,10 @@ def oparams(oracle):
 def sd():
     import paper_1711_03637_b200 as sd
     return sd
+
+
+@pytest.fixture(scope="session")
+def toy():
+    """oracle/gen_toy.py: the reference's two-class convergence corpus and its
+    lateral-inhibition corpus, with the reference's own results."""
+    return dict(np.load(os.path.join(os.path.dirname(GOLD), "toy_reference.npz")))

@@ -386,3 +386,34 @@ def test_hidden_kernel_variants_identical(sd, cfg, bank, workloads, wfix):
             eng.lib.snn_set_normad_cluster(1)
     rel = np.abs(res[0] - res[1]).max() / np.abs(res[1]).max()
     assert rel <= 1e-12, rel   # G summed per shard vs sequentially: last-bit differences only
+
+
+# ------------------------------------------------------------------ mirrors of reference tests
+
+def test_two_class_toy_reaches_perfect_accuracy(sd, cfg, bank, toy):
+    """test_normad.py:236-247 (TestConvergence): 5 epochs of train_epoch on the
+    20-image two-class corpus from zero weights reach 0 errors; the GPU run
+    also reproduces the reference's per-epoch error counts and weights."""
+    learn = sd.LearnConfig()
+    w = sd.zero_weights()
+    errors = []
+    for order in toy["toy_orders"]:
+        w, stats = sd.train_epoch(toy["toy_images"][order], toy["toy_labels"][order], w, bank, cfg, learn)
+        errors.append(stats.n_errors)
+    assert errors[-1] == 0
+    assert errors == toy["toy_errors"].tolist()
+    rel = np.abs(w - toy["toy_w"]).max() / np.abs(toy["toy_w"]).max()
+    assert rel <= 1e-12, rel
+
+
+def test_lateral_inhibition_never_helps_non_winners(sd, cfg, bank, toy):
+    """test_network.py:244-258: with lateral inhibition no non-winner count
+    exceeds its inhibition-free count; both runs equal the reference's."""
+    no_inh = dataclasses.replace(cfg, inhibition_weight=0.0)
+    w = toy["inh_w"]
+    with_c = np.stack([sd.run_presentation(im, w, bank, cfg) for im in toy["inh_images"]])
+    without_c = sd.batch_counts(toy["inh_images"], w, bank, no_inh)
+    assert np.array_equal(with_c, toy["inh_with"]) and np.array_equal(without_c, toy["inh_without"])
+    for a, b in zip(with_c, without_c):
+        winner = int(np.argmax(a))
+        assert all(a[l] <= b[l] for l in range(10) if l != winner)

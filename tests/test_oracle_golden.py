@@ -103,3 +103,24 @@ def test_desired_steps(oracle):
 
 def test_default_inhibition(oracle, oparams):
     assert oparams.inhibition == -5.092904083446687e-08
+
+
+def test_toy_two_class_convergence(oracle, oparams, toy):
+    """test_normad.py:236-247 on the oracle: per-epoch errors and weights."""
+    w = np.zeros((8112, 10))
+    errors = []
+    for order in toy["toy_orders"]:
+        labs = toy["toy_labels"][order]
+        w, counts = oracle.train_epoch(toy["toy_images"][order], labs, w, oparams)
+        errors.append(int(sum(oracle.classify(c) != l for c, l in zip(counts, labs))))
+    assert errors == toy["toy_errors"].tolist() and errors[-1] == 0
+    np.testing.assert_allclose(w, toy["toy_w"], rtol=1e-10, atol=1e-22)
+
+
+def test_lateral_inhibition_corpus(oracle, oparams, toy):
+    """test_network.py:244-258 on the oracle: counts with and without inhibition."""
+    no_inh = dataclasses.replace(oparams, inh=0.0)
+    ctab = oracle.input_table(oparams)[1]
+    for k, im in enumerate(toy["inh_images"]):
+        assert np.array_equal(oracle.simulate(im, toy["inh_w"], oparams, ctab=ctab)["counts"], toy["inh_with"][k])
+        assert np.array_equal(oracle.simulate(im, toy["inh_w"], no_inh, ctab=ctab)["counts"], toy["inh_without"][k])
