@@ -430,6 +430,34 @@ def committed_traffic(prefix):
     return None, None
 
 
+def train_chunks(eng, c, n):
+    """Chunks of one snn_train call (a 64-image first chunk, then full ones)."""
+    chunk = int(eng.lib.snn_train_chunk(ctypes.byref(c), n))
+    if n <= chunk:
+        return 1
+    first = min(chunk, 64)
+    return 1 + -(-(n - first) // chunk)
+
+
+def critical_path_model(c):
+    """Per-image latency floor of the sequential NormAD chain:
+    the output scan's dependent chain per step (no output spike: 6 FP64 ops
+    of 8.2 cycles + threshold test, ballot and select ~25 cycles; after an
+    output spike, 23% of steps, + bumps, difference and the 5-level pairwise
+    sum: 8 more FP64 ops) and the R adjoint's (DMUL -> DADD per step), at the
+    max SM clock; cluster barriers, the DSMEM gather and dW are not counted.
+    Latencies from scripts/scan_micro.py (FP64 dependent op 8.2 cycles)."""
+    n = c.n_steps
+    lat = 8.2
+    scan = 0.77 * (6 * lat + 25) + 0.23 * (14 * lat + 25)
+    adj = 2 * lat
+    cyc = n * (scan + adj)
+    return {"model_us_per_image": cyc / 1965.0, "scan_cycles_per_step": scan, "adjoint_cycles_per_step": adj,
+            "n_steps": n, "clock_mhz": 1965,
+            "basis": "dependent-chain latency only (FP64 8.2 cycles); measured scan alone: 232 cycles/step "
+                     "(issue-bound single warp, scripts/scan_micro.py)"}
+
+
 def bench_train(args, sd, eng, d, cfg, bank):
     import torch
     from paper_1711_03637_b200.engine import make_consts
@@ -472,7 +500,8 @@ def bench_train(args, sd, eng, d, cfg, bank):
             "e2e": {"value": e2e, "unit": "images/s", "api": "train_epoch (host numpy in/out)"},
             "w_rel_err_vs_reference_epoch": rel, "train_errors": stats.n_errors,
             "dense_equiv_tflops": value * (F_TRAIN_PER_STEP * 100 + F_TRAIN_PER_IMAGE) / 1e12,
-            "gpu_launches_per_epoch": 3 * 1,
+            "gpu_launches_per_epoch": 6 * train_chunks(eng, c, n),
+            "critical_path": critical_path_model(c),
             "cpu_baseline": {"value": cpu, "unit": "images/s", "cores": 1, "kind": "port",
                              "sample": f"oracle.train_epoch on the first {k} images (1 core, as the reference)"}}
 

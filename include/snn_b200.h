@@ -152,6 +152,14 @@ void snn_normad_phase_clocks(long long *d_clk);
  * Effective only in the profiling build, like snn_normad_phase_clocks. */
 void snn_normad_skip(int mask);
 
+/* Images per NormAD launch chunk of an n-image snn_train call; 0 for
+ * invalid arguments.  Each chunk runs 6 kernels (prep, tile scan, hidden,
+ * compact, shard, NormAD).  When n exceeds one chunk, the first chunk is
+ * min(chunk, 64) images and the preparation of chunk k+1 runs on an
+ * auxiliary stream during chunk k's NormAD kernel (two workspace buffer
+ * sets, see snn_train_workspace). */
+int64_t snn_train_chunk(const snn_consts_t *c, int64_t n_images);
+
 /* Bytes of device workspace snn_train needs for n images. */
 size_t snn_train_workspace(const snn_consts_t *c, int64_t n_images);
 

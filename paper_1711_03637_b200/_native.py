@@ -75,6 +75,7 @@ SIGNATURES = [
     ("snn_set_hidden_resident", None, [ctypes.c_int]),
     ("snn_normad_phase_clocks", None, [_vp]),
     ("snn_normad_skip", None, [ctypes.c_int]),
+    ("snn_train_chunk", ctypes.c_int64, [ctypes.POINTER(ConstsC), ctypes.c_int64]),
     ("snn_train_workspace", ctypes.c_size_t, [ctypes.POINTER(ConstsC), ctypes.c_int64]),
     ("snn_train", ctypes.c_int, [ctypes.POINTER(ConstsC), _vp, _vp, ctypes.c_int64, _vp, _vp, _vp,
                                  _vp, _vp, ctypes.c_size_t, _vp]),

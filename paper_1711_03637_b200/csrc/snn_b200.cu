@@ -249,6 +249,26 @@ struct Pipe {
 std::mutex g_pipe_mu;
 Pipe g_pipes[64];
 
+// Per-device auxiliary stream + events of snn_train's chunk preparation.
+struct TrainPipe {
+    cudaStream_t aux = nullptr;
+    cudaEvent_t fork = nullptr, pre[2] = {}, done[2] = {};
+};
+TrainPipe g_tpipes[64];
+
+TrainPipe *train_pipe_for_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    TrainPipe &p = g_tpipes[dev];
+    if (!p.aux) {
+        if (cudaStreamCreateWithFlags(&p.aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        for (cudaEvent_t *e : {&p.fork, &p.pre[0], &p.pre[1], &p.done[0], &p.done[1]})
+            if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    }
+    return &p;
+}
+
 Pipe *pipe_for_device() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
@@ -382,9 +402,16 @@ extern "C" void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_pe
     g_hid_ctas = hidden_ctas_per_sm;
 }
 
+extern "C" int64_t snn_train_chunk(const snn_consts_t *c, int64_t n) {
+    if (!c || n <= 0 || c->n_steps <= 0) return 0;
+    return train_chunk(c, n);
+}
+
 extern "C" size_t snn_train_workspace(const snn_consts_t *c, int64_t n) {
     if (!c || n < 0 || c->n_steps <= 0) return 0;
-    return train_ws(c, train_chunk(c, n), nullptr, nullptr);
+    const int64_t chunk = train_chunk(c, n);
+    const size_t one = train_ws(c, chunk, nullptr, nullptr);
+    return n > chunk ? 2 * one : one;  // two chunk buffers: the next chunk is prepared during this one
 }
 
 extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const uint8_t *d_labels, int64_t n,
@@ -425,8 +452,23 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     T.c = *c;
     T.w = d_w;
     T.status = d_status;
-    for (int64_t i0 = 0; i0 < n; i0 += chunk) {
-        const int64_t cn = std::min(chunk, n - i0);
+    // Chunk k's preparation (hidden raster, compaction, shard lists) does not
+    // depend on the weights, so with more than one chunk it runs on an
+    // auxiliary stream into the other buffer set while chunk k-1's NormAD
+    // kernel (8 SMs) runs on the caller's stream.
+    TrainArgs Tb[2] = {T, T};
+    ShardWS Sb[2] = {SW, SW};
+    const bool two = n > chunk;
+    if (two) {
+        const size_t one = train_ws(c, chunk, nullptr, nullptr);
+        if (ws_bytes < 2 * one) return set_error(SNN_ENOMEM, "workspace too small");
+        train_ws(c, chunk, &Tb[1].ws, (char *)d_ws + one, &Sb[1]);
+        Sb[1].clk = SW.clk;
+        Sb[1].push = SW.push;
+        Sb[1].skip = SW.skip;
+    }
+    auto prepare = [&](int64_t i0, int64_t cn, int b, cudaStream_t st) -> int {
+        TrainArgs &U = Tb[b];
         BatchArgs A;
         memset(&A, 0, sizeof(A));
         A.c = *c;
@@ -434,30 +476,62 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
         A.n_images = cn;
         A.w = d_w;
         A.ctab = d_ctab;
-        A.raster = T.ws.raster;
-        A.tile_pos = T.ws.tile_pos;
-        A.n_tiles = T.ws.n_tiles;
-        A.tile_base = T.ws.tile_base;
-        A.n_win = T.ws.n_win;
-        A.win_base = T.ws.win_base;
+        A.raster = U.ws.raster;
+        A.tile_pos = U.ws.tile_pos;
+        A.n_tiles = U.ws.n_tiles;
+        A.tile_base = U.ws.tile_base;
+        A.n_win = U.ws.n_win;
+        A.win_base = U.ws.win_base;
         A.items_per_tile = is_default_bank(*c) ? 1 : 2;
-        if ((rc = is_default_bank(*c) ? launch_fast<true>(A, nullptr, s) : launch_fast<false>(A, nullptr, s)))
-            return rc;
-        T.n = cn;
-        T.first = i0;
-        T.labels = d_labels + i0;
-        T.counts = d_counts + i0 * kNO;
-        k_compact<<<(unsigned)cn, kCThreads, 0, s>>>(T);
-        if ((rc = cuda_check("k_compact"))) return rc;
+        int r;
+        if ((r = is_default_bank(*c) ? launch_fast<true>(A, nullptr, st) : launch_fast<false>(A, nullptr, st)))
+            return r;
+        U.n = cn;
+        U.first = i0;
+        U.labels = d_labels + i0;
+        U.counts = d_counts + i0 * kNO;
+        k_compact<<<(unsigned)cn, kCThreads, 0, st>>>(U);
+        if ((r = cuda_check("k_compact"))) return r;
         if (use_cl) {
-            k_shard<<<(unsigned)cn, kShThreads, k_shard_smem(c->n_steps), s>>>(T, SW);
-            if ((rc = cuda_check("k_shard"))) return rc;
-            k_normad_cl<<<kCl, kClThreads, cl_smem, s>>>(T, SW);
-            if ((rc = cuda_check("k_normad_cl"))) return rc;
-        } else {
-            k_normad<<<1, kTThreads, smem, s>>>(T, caps);
-            if ((rc = cuda_check("k_normad"))) return rc;
+            k_shard<<<(unsigned)cn, kShThreads, k_shard_smem(c->n_steps), st>>>(U, Sb[b]);
+            if ((r = cuda_check("k_shard"))) return r;
         }
+        return SNN_OK;
+    };
+    auto normad = [&](int b, cudaStream_t st) -> int {
+        if (use_cl) {
+            k_normad_cl<<<kCl, kClThreads, cl_smem, st>>>(Tb[b], Sb[b]);
+            return cuda_check("k_normad_cl");
+        }
+        k_normad<<<1, kTThreads, smem, st>>>(Tb[b], caps);
+        return cuda_check("k_normad");
+    };
+    if (!two) {
+        if ((rc = prepare(0, n, 0, s))) return rc;
+        return normad(0, s);
+    }
+    TrainPipe *tp = train_pipe_for_device();
+    if (!tp) return set_error(SNN_ECUDA, "could not create the training streams");
+    cudaEventRecord(tp->fork, s);  // inputs written on the caller's stream
+    cudaStreamWaitEvent(tp->aux, tp->fork, 0);
+    // a short first chunk: only its preparation is exposed
+    const int64_t first = std::min<int64_t>(chunk, 64);
+    int64_t k = 0;
+    if ((rc = prepare(0, first, 0, tp->aux))) return rc;
+    cudaEventRecord(tp->pre[0], tp->aux);
+    for (int64_t i0 = 0; i0 < n; ++k) {
+        const int b = (int)(k & 1);
+        cudaStreamWaitEvent(s, tp->pre[b], 0);
+        if ((rc = normad(b, s))) return rc;
+        cudaEventRecord(tp->done[b], s);
+        const int64_t i1 = i0 + (k == 0 ? first : chunk);
+        if (i1 < n) {
+            const int b1 = b ^ 1;
+            if (k >= 1) cudaStreamWaitEvent(tp->aux, tp->done[b1], 0);  // chunk k-1 is done with buffer b1
+            if ((rc = prepare(i1, std::min(chunk, n - i1), b1, tp->aux))) return rc;
+            cudaEventRecord(tp->pre[b1], tp->aux);
+        }
+        i0 = i1;
     }
     return SNN_OK;
 }
