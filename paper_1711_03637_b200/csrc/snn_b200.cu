@@ -512,6 +512,10 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     }
     TrainPipe *tp = train_pipe_for_device();
     if (!tp) return set_error(SNN_ECUDA, "could not create the training streams");
+    // one call's enqueue sequence at a time: calls from several host threads
+    // share the auxiliary stream and events (each has its own workspace)
+    static std::mutex train_mu;
+    std::lock_guard<std::mutex> lk(train_mu);
     cudaEventRecord(tp->fork, s);  // inputs written on the caller's stream
     cudaStreamWaitEvent(tp->aux, tp->fork, 0);
     // a short first chunk: only its preparation is exposed
