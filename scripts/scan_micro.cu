@@ -399,6 +399,217 @@ __global__ void k_probe(int mode, int iters, long long *cyc, double *out) {
     out[lane] = x + idx;
     if (lane == 0) cyc[0] = t1 - t0;
 }
+// ---- two-warp scan: warp 0 (driver) runs the output LIF chain, warp 1
+// (speculator) turns the spikes of step s-1 into the inhibition sums of step
+// s+1 for the no-spike case (S0) and every single-spike case (S1[q]).  The
+// two talk through shared memory: each value slot is written once and read
+// by polling (a NaN sentinel marks "not yet").
+constexpr int kS2Max = 128;
+constexpr unsigned long long kSent = 0x7FF8DEAD0000BEEFull;
+struct Scan2Smem {
+    double sum[kS2Max + 1][11];
+    double cc[2][2][kNO];  // driver: each trace's c0 / c1 candidates, by step parity (multi-spike steps)
+    unsigned pm[kS2Max + 1];
+};
+
+__device__ __forceinline__ double poll_f64(const double *p) {
+    const volatile long long *q = reinterpret_cast<const volatile long long *>(p);
+    long long x;
+    do {
+        x = *q;
+    } while (x == (long long)kSent);
+    return __longlong_as_double(x);
+}
+__device__ __forceinline__ unsigned poll_u32(const unsigned *p) {
+    const volatile unsigned *q = p;
+    unsigned x;
+    do {
+        x = *q;
+    } while (x == 0xFFFFFFFFu);
+    return x;
+}
+__device__ __forceinline__ void post_f64(double *p, double v) { *reinterpret_cast<volatile double *>(p) = v; }
+__device__ __forceinline__ void post_u32(unsigned *p, unsigned v) { *reinterpret_cast<volatile unsigned *>(p) = v; }
+
+// driver: lane l = output neuron l (lanes >= 10 shadow neuron 9)
+__device__ __forceinline__ int scan2_driver(const snn_consts_t &c, const double *gp, int N, Scan2Smem &X,
+                                            uint16_t *om, double *v_out) {
+    const int lane = threadIdx.x & 31, l = lane < kNO ? lane : kNO - 1;
+    const double lam1 = c.decay_slow, lam2 = c.decay_fast, inh = c.inhibition;
+    const double el = c.lif_out.el, vt = c.lif_out.vt, g = c.lif_out.g, beta = c.lif_out.beta, refr = c.lif_out.refr;
+    double Af = 0.0, Bf = 0.0, v = el, al = 0.0, bl = 0.0, ap = 1.0, bp = 1.0, c0 = 0.0, c1 = 0.0;
+    int live_from = 0, cnt = 0;
+    unsigned prev = 0u;
+    for (int s = 0; s < N; ++s) {
+        const double G = gp[s * kNO];
+        Af = __dadd_rn(__dmul_rn(Af, lam1), G);
+        Bf = __dadd_rn(__dmul_rn(Bf, lam2), G);
+        const double ff = __dsub_rn(Af, Bf);
+        const unsigned pv = prev;
+        const bool mine = (pv >> l) & 1u;
+        const double c0c = c0, c1c = c1;  // this step's own candidates
+        const double co = mine ? c1c : c0c;
+        // own trace into the next step
+        const double a = mine ? ap : al, b = mine ? bp : bl;
+        al = __dmul_rn(a, lam1);
+        bl = __dmul_rn(b, lam2);
+        c0 = __dsub_rn(al, bl);
+        ap = __dadd_rn(al, 1.0);
+        bp = __dadd_rn(bl, 1.0);
+        c1 = __dsub_rn(ap, bp);
+        double S;
+        if (s == 0) {
+            S = 0.0;
+        } else if (pv == 0u) {
+            S = poll_f64(&X.sum[s][0]);
+        } else if ((pv & (pv - 1u)) == 0u) {
+            S = poll_f64(&X.sum[s][__ffs((int)pv)]);
+        } else {  // two or more spikes: the sum with their bumps
+            __syncwarp();
+            const double *cc = &X.cc[s & 1][0][0];
+            double x[kNO];
+#pragma unroll
+            for (int k = 0; k < kNO; ++k) x[k] = cc[(((pv >> k) & 1u) ? kNO : 0) + k];
+            S = pairwise10(x);
+        }
+        if (lane < kNO) {  // the next step's candidates, for a multi-spike step
+            X.cc[(s + 1) & 1][0][lane] = c0;
+            X.cc[(s + 1) & 1][1][lane] = c1;
+        }
+        const double drive = __dadd_rn(ff, __dmul_rn(inh, __dsub_rn(S, co)));
+        double t = __dsub_rn(v, el);
+        t = __dmul_rn(g, t);
+        t = __dsub_rn(drive, t);
+        t = __dmul_rn(beta, t);
+        const double vn = __dadd_rn(v, t);
+        const bool live = s >= live_from;
+        const bool fired = live && vn >= vt;
+        v = (!live || fired || vn < el) ? el : vn;
+        if (fired) live_from = next_live_step(s, refr);
+        prev = __ballot_sync(kFull, fired) & 0x3FFu;
+        cnt += fired ? 1 : 0;
+        if (lane == 0) {
+            post_u32(&X.pm[s + 1], prev);
+            om[s] = (uint16_t)prev;
+        }
+    }
+    if (lane < kNO) v_out[lane] = v;
+    return cnt;
+}
+
+// speculator: lane q < 10 owns trace q; lanes 10 + q form the single-spike sums
+__device__ __forceinline__ void scan2_spec(const snn_consts_t &c, int N, Scan2Smem &X, char *xbuf) {
+    const int lane = threadIdx.x & 31;
+    const double lam1 = c.decay_slow, lam2 = c.decay_fast;
+    DistState st;
+    dist_init(st, c, xbuf, lane);
+    const int q = lane < kNO ? lane : kNO - 1;
+    for (int s = 0; s + 1 < N; ++s) {
+        const unsigned pv = poll_u32(&X.pm[s]);
+        const bool mine = (pv >> q) & 1u;
+        const double a = mine ? st.ap : st.al, b = mine ? st.bp : st.bl;
+        st.al = __dmul_rn(a, lam1);
+        st.bl = __dmul_rn(b, lam2);
+        st.c0 = __dsub_rn(st.al, st.bl);
+        st.ap = __dadd_rn(st.al, 1.0);
+        st.bp = __dadd_rn(st.bl, 1.0);
+        st.c1 = __dsub_rn(st.ap, st.bp);
+        const unsigned nxt = (st.cur & 256u) ? st.cur - 256u : st.cur + 256u;
+        st.cur = nxt;
+        sts64(nxt + st.w0a, st.c0);
+        sts64(nxt + st.w0b, st.c0);
+        sts64(nxt + st.w1, st.c1);
+        __syncwarp();
+        double x[kNO];
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {
+            const double2 p = lds128(nxt + st.rd[m]);
+            x[2 * m] = p.x;
+            x[2 * m + 1] = p.y;
+        }
+        const double T = pairwise10(x);
+        if (lane == 0) post_f64(&X.sum[s + 1][0], T);
+        else if (lane >= kNO && lane < 2 * kNO) post_f64(&X.sum[s + 1][1 + lane - kNO], T);
+    }
+}
+
+__global__ void __launch_bounds__(128) k_scan2(snn_consts_t c, const double *G, int n_img, int32_t *counts, long long *cyc,
+                        uint16_t *om_out, double *v_out) {
+    extern __shared__ double sG[];
+    __shared__ Scan2Smem X;
+    __shared__ __align__(512) char xbuf[kDistSpecBytes];
+    const int N = c.n_steps;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    long long tot = 0;
+    for (int i = 0; i < n_img; ++i) {
+        for (int t = threadIdx.x; t < N * kNO; t += blockDim.x) sG[t] = G[(size_t)i * N * kNO + t];
+        for (int t = threadIdx.x; t < (N + 1) * 11; t += blockDim.x)
+            (&X.sum[0][0])[t] = __longlong_as_double((long long)kSent);
+        for (int t = threadIdx.x; t <= N; t += blockDim.x) X.pm[t] = t == 0 ? 0u : 0xFFFFFFFFu;
+        for (int t = threadIdx.x; t < 2 * 2 * kNO; t += blockDim.x) (&X.cc[0][0][0])[t] = 0.0;
+        __syncthreads();
+        if (warp == 0) {
+            const long long t0 = clock64();
+            const int l = lane < kNO ? lane : kNO - 1;
+            const int cnt = scan2_driver(c, sG + l, N, X, om_out + (size_t)i * N, v_out + i * kNO);
+            tot += clock64() - t0;
+            if (lane < kNO) counts[i * kNO + lane] = cnt;
+        } else if (warp == 1) {
+#ifndef NO_SPEC
+            scan2_spec(c, N, X, xbuf);
+#endif
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) cyc[1] = tot;
+}
+
+// cross-warp ping-pong through shared memory (volatile store -> polling load)
+__global__ void k_pingpong(int iters, long long *cyc) {
+    __shared__ unsigned flag[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < 2) flag[threadIdx.x] = 0xFFFFFFFFu;
+    __syncthreads();
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+        if (warp == 0) {
+            if (lane == 0) post_u32(&flag[0], (unsigned)i);
+            unsigned x;
+            do { x = *reinterpret_cast<volatile unsigned *>(&flag[1]); } while (x != (unsigned)i);
+        } else if (warp == 1) {
+            unsigned x;
+            do { x = *reinterpret_cast<volatile unsigned *>(&flag[0]); } while (x != (unsigned)i);
+            if (lane == 0) post_u32(&flag[1], (unsigned)i);
+        }
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+// cross-warp ping-pong through named barriers (producer bar.arrive, consumer bar.sync)
+__global__ void k_pingbar(int iters, long long *cyc, unsigned *sink) {
+    __shared__ unsigned box[2];
+    const int warp = threadIdx.x >> 5;
+    unsigned acc = 0;
+    __syncthreads();
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+        if (warp == 0) {
+            box[0] = i + acc;
+            asm volatile("bar.arrive 1, 64;" ::: "memory");
+            asm volatile("bar.sync 2, 64;" ::: "memory");
+            acc += box[1];
+        } else if (warp == 1) {
+            asm volatile("bar.sync 1, 64;" ::: "memory");
+            const unsigned x = box[0];
+            box[1] = x + 1;
+            asm volatile("bar.arrive 2, 64;" ::: "memory");
+        }
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) { cyc[0] = t1 - t0; sink[0] = acc; }
+}
+
 }  // namespace
 
 extern "C" int micro_lat(double *out, long long *cyc, int iters) {
@@ -416,6 +627,7 @@ extern "C" int micro_scan(const snn_consts_t *c, const double *G, int n_img, int
     case 3: k_scan<3><<<1, threads, sm>>>(*c, G, n_img, counts, cyc, om, v); break;
     case 12: k_scan<12><<<1, threads, sm>>>(*c, G, n_img, counts, cyc, om, v); break;
     case 13: k_scan<13><<<1, threads, sm>>>(*c, G, n_img, counts, cyc, om, v); break;
+    case 4: k_scan2<<<1, threads < 64 ? 64 : threads, sm>>>(*c, G, n_img, counts, cyc, om, v); break;
     default: return -1;
     }
     return (int)cudaDeviceSynchronize();
@@ -423,5 +635,15 @@ extern "C" int micro_scan(const snn_consts_t *c, const double *G, int n_img, int
 
 extern "C" int micro_probe(int mode, int iters, long long *cyc, double *out) {
     k_probe<<<1, 32>>>(mode, iters, cyc, out);
+    return (int)cudaDeviceSynchronize();
+}
+
+extern "C" int micro_pingpong(int iters, long long *cyc) {
+    k_pingpong<<<1, 64>>>(iters, cyc);
+    return (int)cudaDeviceSynchronize();
+}
+
+extern "C" int micro_pingbar(int iters, long long *cyc, unsigned *sink) {
+    k_pingbar<<<1, 64>>>(iters, cyc, sink);
     return (int)cudaDeviceSynchronize();
 }

@@ -46,6 +46,13 @@ for mode, name in enumerate(("LDS.64 chase", "STS+syncwarp+LDS", "DSETP+VOTE+sel
     for _ in range(2):
         lib.micro_probe(mode, iters, ctypes.c_void_p(cyc.data_ptr()), ctypes.c_void_p(out.data_ptr()))
     print(f"probe {name}: {cyc[0].item() / iters:.1f} cycles/iter")
+lib.micro_pingpong(iters, ctypes.c_void_p(cyc.data_ptr()))
+lib.micro_pingpong(iters, ctypes.c_void_p(cyc.data_ptr()))
+print(f"cross-warp ping-pong (shared memory flag): {cyc[0].item() / iters:.1f} cycles per round trip")
+sink = torch.zeros(4, dtype=torch.int32, device="cuda")
+for _ in range(2):
+    lib.micro_pingbar(iters, ctypes.c_void_p(cyc.data_ptr()), ctypes.c_void_p(sink.data_ptr()))
+print(f"cross-warp ping-pong (named barriers): {cyc[0].item() / iters:.1f} cycles per round trip")
 N = cfg.n_steps
 VARIANTS = [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["0", "1"])]
 res = {}
