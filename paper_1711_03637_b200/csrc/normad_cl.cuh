@@ -67,7 +67,7 @@ struct ShardWS {
     int32_t *nbase;   // [n][kCl + 1]      start of each shard's spike block in snsp
     uint16_t *snsp;   // [n][evcap]        shard-major spike steps of the active neurons
     double *undo;     // [kCl][kClRows][10] old rows of the last committed image
-    int push;         // partials / R pushed through DSMEM stores (normad_cl_smem_bytes)
+    int push;         // G partials pushed to the leader through DSMEM stores (normad_cl_smem_bytes)
     int skip;         // profiling only (snn_normad_skip): bit 0 scan, 1 R, 2 dW, 3 G partials, 4 gather
 };
 
@@ -87,12 +87,13 @@ __host__ __device__ inline size_t cl_buf_bytes(int N) {
 }
 
 // push: every CTA stores its G partials straight into the leader's shared
-// memory (and the leader stores R into every CTA's), so no CTA reads remote
-// shared memory on the serial path; needs kCl partial buffers on the leader.
+// memory, so the leader reads no remote shared memory on the serial path;
+// needs kCl partial buffers on the leader.  (R is not transferred: the leader
+// sends the output spikes and every CTA derives sigma and R itself.)
 __host__ __device__ inline size_t normad_cl_smem_bytes(int N, bool push) {
     return (size_t)kClRows * kNO * 8          // W shard
-           + (size_t)N * kNO * 8 * 3          // P (G on the leader), R copy, R (leader)
-           + (size_t)N * 8                    // q (leader)
+           + (size_t)N * kNO * 8 * 2          // P (G on the leader), sigma -> R
+           + (size_t)N * 8                    // q
            + (size_t)N * 2 + 64 + 16          // OMASK, flags
            + 2 * ((cl_buf_bytes(N) + 15) & ~(size_t)15)
            + (push ? (size_t)kCl * N * kNO * 8 : 0);  // the partials of every CTA (leader)
@@ -258,9 +259,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
     const TrainWS &W = T.ws;
     double *Wsh = csm;                          // [kClRows][10]
     double *P = Wsh + (size_t)kClRows * kNO;    // [N][10] partial G (leader: G)
-    double *Rl = P + (size_t)N * kNO;           // [N][10] local copy of R
-    double *SR = Rl + (size_t)N * kNO;          // [N][10] leader: sigma, then R in place
-    double *Q = SR + (size_t)N * kNO;           // [N] leader: dt / |d_hat|
+    double *SR = P + (size_t)N * kNO;           // [N][10] sigma, then R in place
+    double *Q = SR + (size_t)N * kNO;           // [N] dt / |d_hat|
     uint16_t *OMASK = reinterpret_cast<uint16_t *>(Q + N);
     int *flags = reinterpret_cast<int *>(OMASK + ((N + 7) & ~7));  // leader: per-CTA non-finite flags
     uint8_t *bufmem = reinterpret_cast<uint8_t *>(flags + 16);
@@ -268,7 +268,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
     double *PQ = reinterpret_cast<double *>(bufmem + 2 * bstride);  // leader, push: [kCl][N][10]
     const bool push = SW.push != 0;
     __shared__ ClBuf s_buf[2];
-    __shared__ int s_abort;
+    __shared__ int s_abort, s_label;
 
     const int rows = cl_rows(r);
     if (T.status[0] != 0) return;  // an earlier chunk failed (uniform over the cluster)
@@ -276,7 +276,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
     for (int t = tid; t < rows * kNO; t += kClThreads)
         Wsh[t] = __ldcg(T.w + (size_t)cl_id(r, t / kNO) * kNO + t % kNO);
     if (tid < kCl) flags[tid] = 0;
-    const double *SR_lead = cluster.map_shared_rank(SR, 0);
     double *PQ_lead = cluster.map_shared_rank(PQ, 0) + (size_t)r * N * kNO;  // this CTA's partials there
     int *flags_lead = cluster.map_shared_rank(flags, 0);
 
@@ -399,7 +398,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
                 for (int q = 1; q < kCl; ++q) g = __dadd_rn(g, v[q]);
                 P[t] = g;
             }
-            for (int s = tid; s < N; s += kClThreads) Q[s] = SW.q[(size_t)i * N + s];
             __syncthreads();
             stamp(3);
             if (warp == 0) {
@@ -419,57 +417,60 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
 #ifdef SNN_NORMAD_PROFILE
                 if (clk && lane == 0) clk[12] = clock64();
 #endif
-            } else if (more) {
-                stage(i + 1, (int)((i + 1) & 1), 32, kClThreads - 32);
+            } else {
+                // this image's gate values and label, off the chain; the next image's lists
+                for (int s = tid - 32; s < N; s += kClThreads - 32) Q[s] = SW.q[(size_t)i * N + s];
+                if (tid == 32) s_label = T.labels[i];
+                if (more) stage(i + 1, (int)((i + 1) & 1), 32, kClThreads - 32);
 #ifdef SNN_NORMAD_PROFILE
                 if (clk && lane == 0) atomicMax((unsigned long long *)&clk[13], (unsigned long long)clock64());
 #endif
             }
             __syncthreads();
             stamp(4);
-            // error signal and gate (normad.py:156-159, :87-91, :104-113): the step
-            // counts when some e != 0 and |d_hat| > eps; sigma = e * dt / |d_hat| =
-            // +-(dt / |d_hat|) (IEEE division is sign-symmetric)
-            {
-                const int label = T.labels[i];
-                const int per = c.desired_period;
-                for (int t = tid; t < N * kNO; t += kClThreads) {
-                    const int s = t / kNO, l = t - s * kNO;
-                    const bool want = per > 0 && (s + 1) % per == 0 && l == label;  // network.py:191-193
-                    const bool got = (OMASK[s] >> l) & 1u;
-                    const double q = Q[s];
-                    SR[t] = want == got ? 0.0 : (want ? q : -q);
-                }
+            // the output spikes to every CTA: each derives sigma and R itself
+            for (int t = tid; t < (kCl - 1) * N; t += kClThreads) {
+                const int q = 1 + t / N, s = t - (q - 1) * N;
+                cluster.map_shared_rank(OMASK, q)[s] = OMASK[s];
             }
-            __syncthreads();
-            stamp(5);
-            // R(u, l) = sum_{s >= u} sigma(s, l) H(s - u): adjoint of kernel -> d_hat, backward
-            if (warp == 0 && lane < kNO) {
-                double pd = 0.0, pa = 0.0, pb = 0.0;
-                for (int u = (skip & 2) ? -1 : N - 1; u >= 0; --u) {
-                    pd = __dadd_rn(__dmul_rn(pd, c.decay_learn), SR[u * kNO + lane]);
-                    const double q = __dmul_rn(pd, c.dhat_scale);
-                    pa = __dadd_rn(__dmul_rn(pa, c.decay_slow), q);
-                    pb = __dadd_rn(__dmul_rn(pb, c.decay_fast), q);
-                    SR[u * kNO + lane] = __dsub_rn(pa, pb);
-                }
-            }
-            __syncthreads();
-            stamp(6);
-            if (push)  // R into every CTA's shared memory
-                for (int t = tid; t < kCl * N * kNO; t += kClThreads) {
-                    const int q = t / (N * kNO), k = t - q * (N * kNO);
-                    cluster.map_shared_rank(Rl, q)[k] = SR[k];
-                }
-        } else if (more) {
-            stage(i + 1, (int)((i + 1) & 1), 0, kClThreads);
+        } else {
+            for (int s = tid; s < N; s += kClThreads) Q[s] = SW.q[(size_t)i * N + s];
+            if (tid == 0) s_label = T.labels[i];
+            if (more) stage(i + 1, (int)((i + 1) & 1), 0, kClThreads);
         }
-        cluster.sync();  // B2: R ready on the leader, next lists staged
+        cluster.sync();  // B2: output spikes everywhere, next lists staged
+        stamp(5);
+        // error signal and gate (normad.py:156-159, :87-91, :104-113): the step
+        // counts when some e != 0 and |d_hat| > eps; sigma = e * dt / |d_hat| =
+        // +-(dt / |d_hat|) (IEEE division is sign-symmetric)
+        {
+            const int label = s_label;
+            const int per = c.desired_period;
+            for (int t = tid; t < N * kNO; t += kClThreads) {
+                const int s = t / kNO, l = t - s * kNO;
+                const bool want = per > 0 && (s + 1) % per == 0 && l == label;  // network.py:191-193
+                const bool got = (OMASK[s] >> l) & 1u;
+                const double q = Q[s];
+                SR[t] = want == got ? 0.0 : (want ? q : -q);
+            }
+        }
+        __syncthreads();
+        stamp(6);
+        // R(u, l) = sum_{s >= u} sigma(s, l) H(s - u): adjoint of kernel -> d_hat,
+        // backward; every CTA runs it on its own copy (no R transfer)
+        if (warp == 0 && lane < kNO) {
+            double pd = 0.0, pa = 0.0, pb = 0.0;
+            for (int u = (skip & 2) ? -1 : N - 1; u >= 0; --u) {
+                pd = __dadd_rn(__dmul_rn(pd, c.decay_learn), SR[u * kNO + lane]);
+                const double q = __dmul_rn(pd, c.dhat_scale);
+                pa = __dadd_rn(__dmul_rn(pa, c.decay_slow), q);
+                pb = __dadd_rn(__dmul_rn(pb, c.decay_fast), q);
+                SR[u * kNO + lane] = __dsub_rn(pa, pb);
+            }
+        }
+        __syncthreads();
         stamp(7);
-        if (!push) {
-            for (int t = tid; t < N * kNO; t += kClThreads) Rl[t] = SR_lead[t];
-            __syncthreads();
-        }
+        const double *Rloc = SR;
         stamp(8);
         // dW for the shard's active neurons (spikes ascending); commit with an undo log
         bool bad = false;
@@ -480,7 +481,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
             for (int l = 0; l < kNO; ++l) acc[l] = 0.0;
             const int e1 = B.aoff[a + 1];
             for (int e = B.aoff[a]; e < e1; ++e) {
-                const double *rr = Rl + (int)B.nsp[e] * kNO;
+                const double *rr = Rloc + (int)B.nsp[e] * kNO;
 #pragma unroll
                 for (int l = 0; l < kNO; ++l) acc[l] = __dadd_rn(acc[l], rr[l]);
             }

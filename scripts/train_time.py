@@ -15,6 +15,8 @@ order = d["c2_order"]
 imgs = torch.from_numpy(d["c2_images"][order].reshape(1000, -1).copy()).cuda()
 labs = torch.from_numpy(d["c2_labels"][order].astype(np.uint8)).cuda()
 dw = torch.zeros((8112, 10), dtype=torch.float64, device="cuda")
+if os.environ.get("SNN_CLUSTER_MODE"):
+    eng.lib.snn_set_normad_cluster(int(os.environ["SNN_CLUSTER_MODE"]))
 ts = []
 for rep in range(8):
     dw.zero_()
