@@ -172,6 +172,20 @@ int snn_train(const snn_consts_t *c, const uint8_t *d_images, const uint8_t *d_l
               int64_t n_images, double *d_weights, const double *d_ctab, int32_t *d_counts,
               int32_t *d_status, void *d_workspace, size_t workspace_bytes, void *stream);
 
+/* Canvas preprocessing (replaces preprocess.preprocess_pipeline,
+ * /root/reference/pkg/src/spikedigits/preprocess.py:110-115): n grayscale
+ * canvases of any shape up to 1024 x 1024, row-major uint8, back to back in
+ * d_pixels (canvas i starts at d_offsets[i], shape d_shapes[2i] x
+ * d_shapes[2i+1], ink threshold d_thresholds[i] in 0..255) -> d_out
+ * [n][28][28] uint8, bit-identical to the reference (binarize, crop to ink,
+ * Pillow BILINEAR resize of the longer side to 20, centre of mass, 3x3
+ * Gaussian blur).  blur3x3 (host, 9 doubles) is the reference's normalised
+ * kernel.  d_status[i]: 0 ok, 1 blank drawing (BlankDrawingError), 2 shape
+ * outside 1..1024.  One CTA per canvas. */
+int snn_preprocess(const uint8_t *d_pixels, const int64_t *d_offsets, const int32_t *d_shapes,
+                   const int32_t *d_thresholds, int64_t n, const double *blur3x3, uint8_t *d_out,
+                   int32_t *d_status, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

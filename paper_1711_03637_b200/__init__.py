@@ -8,6 +8,7 @@ or call ``paper_1711_03637_b200.shim.install()`` to reroute an installed
 """
 from .api import (EvalReport, batch_counts, batch_counts_device, evaluate_dataset, forward_pass,
                   run_presentation, train_epoch, train_presentation)
+from .preprocess import BlankDrawingError, preprocess_batch, preprocess_pipeline
 from .params import (DEFAULT_FILTER_DRIVE, DEFAULT_LEARNING_RATE, N_HIDDEN, N_INPUTS, N_OUTPUTS,
                      EncodingParams, EpochStats, FilterBank, LearnConfig, LifParams, NetworkConfig,
                      NumericFailureError, SpikeRecord, as_pixel_batch, as_pixel_image, check_weights,
@@ -23,4 +24,5 @@ __all__ = [
     "default_filter_bank", "desired_spike_train", "min_spiking_current", "parameter_count",
     "single_synapse_rate_weight", "zero_weights", "as_pixel_batch", "as_pixel_image", "check_weights",
     "N_HIDDEN", "N_INPUTS", "N_OUTPUTS", "DEFAULT_FILTER_DRIVE", "DEFAULT_LEARNING_RATE",
+    "preprocess_pipeline", "preprocess_batch", "BlankDrawingError",
 ]

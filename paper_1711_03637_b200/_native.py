@@ -77,6 +77,7 @@ SIGNATURES = [
     ("snn_normad_skip", None, [ctypes.c_int]),
     ("snn_train_chunk", ctypes.c_int64, [ctypes.POINTER(ConstsC), ctypes.c_int64]),
     ("snn_train_workspace", ctypes.c_size_t, [ctypes.POINTER(ConstsC), ctypes.c_int64]),
+    ("snn_preprocess", ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp]),
     ("snn_train", ctypes.c_int, [ctypes.POINTER(ConstsC), _vp, _vp, ctypes.c_int64, _vp, _vp, _vp,
                                  _vp, _vp, ctypes.c_size_t, _vp]),
 ]

@@ -7,6 +7,7 @@
 #include <mutex>
 
 #include "normad_cl.cuh"
+#include "preprocess.cuh"
 
 using namespace snn;
 
@@ -538,4 +539,25 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
         i0 = i1;
     }
     return SNN_OK;
+}
+
+extern "C" int snn_preprocess(const uint8_t *d_pixels, const int64_t *d_offsets, const int32_t *d_shapes,
+                              const int32_t *d_thresholds, int64_t n, const double *blur3x3, uint8_t *d_out,
+                              int32_t *d_status, void *stream) {
+    if (n < 0) return set_error(SNN_EINVAL, "n < 0");
+    if (n == 0) return SNN_OK;
+    if (!d_pixels || !d_offsets || !d_shapes || !d_thresholds || !blur3x3 || !d_out || !d_status)
+        return set_error(SNN_EINVAL, "NULL pointer");
+    if (n > 0x7fffffffLL) return set_error(SNN_EINVAL, "too many canvases in one call");
+    PreArgs P;
+    P.pixels = d_pixels;
+    P.offsets = d_offsets;
+    P.shapes = d_shapes;
+    P.thresholds = d_thresholds;
+    P.n = n;
+    for (int k = 0; k < 9; ++k) P.blur[k] = blur3x3[k];
+    P.out = d_out;
+    P.status = d_status;
+    k_preprocess<<<(unsigned)n, kPThreads, 0, (cudaStream_t)stream>>>(P);
+    return cuda_check("k_preprocess");
 }

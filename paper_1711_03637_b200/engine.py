@@ -82,6 +82,7 @@ class Engine:
         self._w_host = None      # host copy of the weights last uploaded by weights()
         self._w_dev = None
         self._graphs: dict = {}  # batch-1 CUDA graphs per configuration (infer_one)
+        self._pinned: dict = {}   # grow-only pinned host staging buffers
 
     # ------------------------------------------------------------ helpers
     @property
@@ -95,6 +96,15 @@ class Engine:
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
             self._ws[name] = buf
+        return buf
+
+    def pinned(self, name: str, nbytes: int):
+        """Grow-only pinned host staging buffer (uint8 tensor)."""
+        torch = _torch()
+        buf = self._pinned.get(name)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 4096), dtype=torch.uint8).pin_memory()
+            self._pinned[name] = buf
         return buf
 
     def table(self, c: _native.ConstsC):

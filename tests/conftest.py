@@ -54,3 +54,12 @@ def toy():
     """oracle/gen_toy.py: the reference's two-class convergence corpus and its
     lateral-inhibition corpus, with the reference's own results."""
     return dict(np.load(os.path.join(os.path.dirname(GOLD), "toy_reference.npz")))
+
+
+@pytest.fixture(scope="session")
+def canvases():
+    """oracle/gen_canvases.py: canvases of many shapes with the reference's
+    preprocess_pipeline outputs (blank ones flagged)."""
+    z = dict(np.load(os.path.join(os.path.dirname(GOLD), "canvases.npz")))
+    z["list"] = [z["pixels"][o:o + h * w].reshape(h, w) for (h, w), o in zip(z["shapes"], z["offsets"][:-1])]
+    return z
