@@ -370,6 +370,7 @@ def run_ours(args):
         line["train"] = bench_train(args, sd, eng, d, cfg, bank)
     if rank == 0 and not args.skip_latency:
         line["latency"] = bench_latency(sd, d, w_fix, bank)
+        line["preprocess"] = bench_preprocess(sd, w_fix, bank)
     if rank == 0 and world == 1 and not args.skip_cpu:
         line["cpu_baseline"] = cpu_baseline(d, w_fix)
     if rank == 0 and not args.skip_c5 and os.path.exists(os.path.join(ROOT, "data", "c5_workload.npz")):
@@ -603,6 +604,55 @@ def bench_latency(sd, d, w_fix, bank):
             "mean_ms": float(ms.mean()), "max_ms": float(ms.max()), "budget_ms": 100.0,
             "api": "run_presentation (host image + host float64 weights each call)",
             "c4_first100_counts_equal_reference": bool(same)}
+
+
+def bench_preprocess(sd, w_fix, bank):
+    """SURVEY 8(f) GPU preprocess: the 500 synthetic user canvases of config 4
+    (tests/golden/canvases.npz, shapes 75-110 px) through preprocess_batch
+    (host canvases in, 28x28 images out, one launch) and, per canvas, the
+    serving path preprocess_pipeline + run_presentation (T = 75 ms) as
+    service.py:146-157 runs it.  Checked against the reference's outputs.
+    CPU baseline: the reference's own pipeline with Pillow's C resize
+    (oracle.preprocess_oracle.preprocess_pil), one core."""
+    import dataclasses
+    from oracle import preprocess_oracle as po
+    z = np.load(os.path.join(ROOT, "tests", "golden", "canvases.npz"))
+    canv = [z["pixels"][o:o + h * w].reshape(h, w) for (h, w), o in zip(z["shapes"][:500], z["offsets"][:500])]
+    want = z["outputs"][:500]
+    for _ in range(3):
+        imgs, blank = sd.preprocess_batch(canv)
+    ts = []
+    for _ in range(10):
+        t0 = time.perf_counter()
+        imgs, blank = sd.preprocess_batch(canv)
+        ts.append(time.perf_counter() - t0)
+    batch_s = statistics.median(ts)
+    cfg75 = dataclasses.replace(sd.NetworkConfig(), t=0.075)
+    for c in canv[:20]:
+        sd.run_presentation(sd.preprocess_pipeline(c), w_fix, bank, cfg75)
+    pre_ms, serve_ms = [], []
+    for c in canv:
+        t0 = time.perf_counter()
+        im = sd.preprocess_pipeline(c)
+        t1 = time.perf_counter()
+        sd.run_presentation(im, w_fix, bank, cfg75)
+        t2 = time.perf_counter()
+        pre_ms.append((t1 - t0) * 1e3)
+        serve_ms.append((t2 - t0) * 1e3)
+    k = 200
+    t0 = time.perf_counter()
+    for c in canv[:k]:
+        po.preprocess_pil(c)
+    cpu = k / (time.perf_counter() - t0)
+    return {"metric": "canvas preprocessing (500 synthetic user canvases -> 28x28), canvases/s", "value": 500 / batch_s,
+            "unit": "canvases/s", "api": "preprocess_batch (host canvases in, images out)",
+            "batch1_preprocess_p50_ms": float(np.percentile(pre_ms, 50)),
+            "serve_p50_ms": float(np.percentile(serve_ms, 50)), "serve_p99_ms": float(np.percentile(serve_ms, 99)),
+            "serve_api": "preprocess_pipeline + run_presentation, T=75 ms (service.py:146-157)",
+            "outputs_equal_reference": bool(np.array_equal(imgs, want) and not blank.any()),
+            "cpu_baseline": {"value": cpu, "unit": "canvases/s", "cores": 1, "kind": "port",
+                             "sample": f"first {k} canvases, the reference pipeline with Pillow's C resize "
+                                       "(oracle.preprocess_oracle.preprocess_pil)"}}
 
 
 def cpu_baseline(d, w):

@@ -94,7 +94,16 @@ def resize_bilinear(img: np.ndarray, new_w: int, new_h: int) -> np.ndarray:
     return np.ascontiguousarray(out)
 
 
-def preprocess(canvas, threshold: int = 128) -> np.ndarray:
+def preprocess_pil(canvas, threshold: int = 128) -> np.ndarray:
+    """The reference's own code path (Pillow's C resize): the CPU baseline
+    bench.py times.  Same outputs as preprocess()."""
+    from PIL import Image
+    return preprocess(canvas, threshold,
+                      resize=lambda img, w, h: np.asarray(Image.fromarray(img).resize((w, h), Image.Resampling.BILINEAR),
+                                                          dtype=np.uint8))
+
+
+def preprocess(canvas, threshold: int = 128, resize=None) -> np.ndarray:
     """preprocess_pipeline (preprocess.py:110-115) -> uint8 [28, 28]."""
     arr = np.asarray(canvas)
     if arr.ndim != 2 or arr.shape[0] < 1 or arr.shape[1] < 1:
@@ -113,7 +122,7 @@ def preprocess(canvas, threshold: int = 128) -> np.ndarray:
         new_h, new_w = CONTENT_SIDE, max(1, int(math.floor(w * CONTENT_SIDE / h + 0.5)))
     else:
         new_w, new_h = CONTENT_SIDE, max(1, int(math.floor(h * CONTENT_SIDE / w + 0.5)))
-    img = resize_bilinear(ink, new_w, new_h)
+    img = (resize or resize_bilinear)(ink, new_w, new_h)
     a = img.astype(np.float64)
     h, w = a.shape
     total = a.sum()

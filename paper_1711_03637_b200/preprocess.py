@@ -13,7 +13,6 @@ side (the service's MAX_CANVAS_SIDE, service.py:31) are rejected.
 from __future__ import annotations
 
 import ctypes
-import threading
 
 import numpy as np
 
@@ -37,7 +36,7 @@ def _blur_kernel(sigma: float = BLUR_SIGMA) -> np.ndarray:
 
 
 _BLUR = _blur_kernel()
-_LOCK = threading.Lock()
+_BLANK_ERROR = BlankDrawingError  # shim.install() points this at the reference's class
 
 
 def _as_canvas(canvas) -> np.ndarray:
@@ -107,7 +106,7 @@ def preprocess_pipeline(canvas, threshold: int = 128) -> np.ndarray:
     """Full canvas-to-28x28 pipeline on the GPU; raises BlankDrawingError on empty ink."""
     images, blank = preprocess_batch([canvas], threshold)
     if blank[0]:
-        raise BlankDrawingError("blank drawing: no ink above threshold")
+        raise _BLANK_ERROR("blank drawing: no ink above threshold")
     return images[0]
 
 

@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import importlib
 
-from . import api
+from . import api, preprocess
 
 # (module, attribute, replacement)
 _BINDINGS = [
@@ -27,6 +27,9 @@ _BINDINGS = [
     ("spikedigits.estimator", "train_epoch", api.train_epoch),
     ("spikedigits", "forward_pass", api.forward_pass),
     ("spikedigits", "train_epoch", api.train_epoch),
+    ("spikedigits.cli", "preprocess_pipeline", preprocess.preprocess_pipeline),
+    ("spikedigits.service", "preprocess_pipeline", preprocess.preprocess_pipeline),
+    ("spikedigits.strokes", "preprocess_pipeline", preprocess.preprocess_pipeline),
 ]
 
 _saved: list = []
@@ -41,6 +44,7 @@ def install() -> int:
     api._NUMERIC_ERROR = normad.NumericFailureError
     api._EPOCH_STATS = normad.EpochStats
     api._SPIKE_RECORD = network.SpikeRecord
+    preprocess._BLANK_ERROR = importlib.import_module("spikedigits.preprocess").BlankDrawingError
     for mod_name, attr, fn in _BINDINGS:
         try:
             mod = importlib.import_module(mod_name)
@@ -60,3 +64,4 @@ def uninstall() -> None:
     api._NUMERIC_ERROR = NumericFailureError
     api._EPOCH_STATS = EpochStats
     api._SPIKE_RECORD = SpikeRecord
+    preprocess._BLANK_ERROR = preprocess.BlankDrawingError

@@ -142,6 +142,12 @@ def test_shim_install_rebinds_reference():
         assert nm.train_epoch is api.train_epoch
         assert sdr.forward_pass is api.forward_pass
         assert api._NUMERIC_ERROR is nm.NumericFailureError
+        import spikedigits.cli as cli
+        import spikedigits.preprocess as rpre
+        from paper_1711_03637_b200 import preprocess as gpre
+        assert cli.preprocess_pipeline is gpre.preprocess_pipeline
+        assert gpre._BLANK_ERROR is rpre.BlankDrawingError
     finally:
         shim.uninstall()
     assert ev.batch_counts is orig
+    assert gpre._BLANK_ERROR is gpre.BlankDrawingError
