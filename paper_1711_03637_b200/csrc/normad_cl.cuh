@@ -68,6 +68,7 @@ struct ShardWS {
     uint16_t *snsp;   // [n][evcap]        shard-major spike steps of the active neurons
     double *undo;     // [kCl][kClRows][10] old rows of the last committed image
     int push;         // G partials pushed to the leader through DSMEM stores (normad_cl_smem_bytes)
+    int alias;        // sigma/R share P's shared memory (long trials; G is dead after the scan)
     int skip;         // profiling only (snn_normad_skip): bit 0 scan, 1 R, 2 dW, 3 G partials, 4 gather
 };
 
@@ -90,9 +91,9 @@ __host__ __device__ inline size_t cl_buf_bytes(int N) {
 // memory, so the leader reads no remote shared memory on the serial path;
 // needs kCl partial buffers on the leader.  (R is not transferred: the leader
 // sends the output spikes and every CTA derives sigma and R itself.)
-__host__ __device__ inline size_t normad_cl_smem_bytes(int N, bool push) {
+__host__ __device__ inline size_t normad_cl_smem_bytes(int N, bool push, bool alias = false) {
     return (size_t)kClRows * kNO * 8          // W shard
-           + (size_t)N * kNO * 8 * 2          // P (G on the leader), sigma -> R
+           + (size_t)N * kNO * 8 * (alias ? 1 : 2)  // P (G on the leader), sigma -> R
            + (size_t)N * 8                    // q
            + (size_t)N * 2 + 64 + 16          // OMASK, flags
            + 2 * ((cl_buf_bytes(N) + 15) & ~(size_t)15)
@@ -259,8 +260,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
     const TrainWS &W = T.ws;
     double *Wsh = csm;                          // [kClRows][10]
     double *P = Wsh + (size_t)kClRows * kNO;    // [N][10] partial G (leader: G)
-    double *SR = P + (size_t)N * kNO;           // [N][10] sigma, then R in place
-    double *Q = SR + (size_t)N * kNO;           // [N] dt / |d_hat|
+    double *SR = SW.alias ? P : P + (size_t)N * kNO;  // [N][10] sigma, then R in place
+    double *Q = P + (size_t)N * kNO * (SW.alias ? 1 : 2);  // [N] dt / |d_hat|
     uint16_t *OMASK = reinterpret_cast<uint16_t *>(Q + N);
     int *flags = reinterpret_cast<int *>(OMASK + ((N + 7) & ~7));  // leader: per-CTA non-finite flags
     uint8_t *bufmem = reinterpret_cast<uint8_t *>(flags + 16);

@@ -430,7 +430,9 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     if (c->n_steps > 65535) return set_error(SNN_EINVAL, "training supports n_steps <= 65535");
     // the W-resident cluster kernel when its shared memory fits, else the one-CTA kernel
     const bool cl_push = g_normad_cluster == 1 && normad_cl_smem_bytes(c->n_steps, true) <= 227 * 1024;
-    const size_t cl_smem = normad_cl_smem_bytes(c->n_steps, cl_push);
+    // long trials: sigma/R reuse the G array, so the cluster kernel fits up to N ~ 1,300
+    const bool cl_alias = !cl_push && normad_cl_smem_bytes(c->n_steps, false) > 227 * 1024;
+    const size_t cl_smem = normad_cl_smem_bytes(c->n_steps, cl_push, cl_alias);
     const bool use_cl = g_normad_cluster && cl_smem <= 227 * 1024;
     const NormadCaps caps = normad_caps(c);
     const size_t smem = normad_smem_bytes(c->n_steps, caps);
@@ -442,6 +444,7 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     const size_t need = train_ws(c, chunk, &T.ws, (char *)d_ws, &SW);
     SW.clk = g_phase_clk;
     SW.push = cl_push ? 1 : 0;
+    SW.alias = cl_alias ? 1 : 0;
     SW.skip = g_normad_skip;
     if (!d_ws || ws_bytes < need) return set_error(SNN_ENOMEM, "workspace too small");
     if (use_cl) {
@@ -466,6 +469,7 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
         train_ws(c, chunk, &Tb[1].ws, (char *)d_ws + one, &Sb[1]);
         Sb[1].clk = SW.clk;
         Sb[1].push = SW.push;
+        Sb[1].alias = SW.alias;
         Sb[1].skip = SW.skip;
     }
     auto prepare = [&](int64_t i0, int64_t cn, int b, cudaStream_t st) -> int {
