@@ -374,17 +374,25 @@ def test_hidden_kernel_variants_identical(sd, cfg, bank, workloads, wfix):
             eng.lib.snn_set_hidden_resident(1)
     for k in outs[0]:
         assert np.array_equal(outs[0][k], outs[1][k]), k
+    # sub-batch pipelining (snn_set_pipeline): same counts
+    eng.lib.snn_set_pipeline(16, 0)
+    try:
+        piped = eng.infer(c, imgs, w)["counts"].cpu().numpy()
+    finally:
+        eng.lib.snn_set_pipeline(0, 0)
+    assert np.array_equal(piped, outs[0]["counts"])
     learn = sd.LearnConfig()
     order = workloads["c2_order"][:40]
     ims, labs = workloads["c2_images"][order], workloads["c2_labels"][order]
     res = []
-    for cl in (1, 0):
+    for cl in (1, 2, 0):  # cluster (partials pushed / pulled) and the one-CTA kernel
         eng.lib.snn_set_normad_cluster(cl)
         try:
             res.append(sd.train_epoch(ims, labs, sd.zero_weights(), bank, cfg, learn)[0])
         finally:
             eng.lib.snn_set_normad_cluster(1)
-    rel = np.abs(res[0] - res[1]).max() / np.abs(res[1]).max()
+    assert np.array_equal(res[0], res[1])  # push and pull: same sums in the same order
+    rel = np.abs(res[0] - res[2]).max() / np.abs(res[2]).max()
     assert rel <= 1e-12, rel   # G summed per shard vs sequentially: last-bit differences only
 
 
