@@ -33,6 +33,17 @@ for i in range(n_img):
     for k, ts in enumerate(rec.hidden_spikes):
         m[ts, k] = 1.0
     Gs.append(m @ w)
+if os.environ.get("SCAN_W_TRAIN"):
+    # weights after 40 online NormAD images from zero (the training regime)
+    wt, _ = sd.train_epoch(d["c2_images"][d["c2_order"][:40]], d["c2_labels"][d["c2_order"][:40]],
+                           sd.zero_weights(), bank, cfg, sd.LearnConfig())
+    Gs = []
+    for i in range(n_img):
+        rec = sd.forward_pass(d["c2_images"][d["c2_order"][40 + i]], wt, bank, cfg)
+        m = np.zeros((cfg.n_steps, 8112))
+        for k, ts in enumerate(rec.hidden_spikes):
+            m[ts, k] = 1.0
+        Gs.append(m @ wt)
 G = torch.from_numpy(np.stack(Gs)).cuda()
 counts = torch.zeros((n_img, 10), dtype=torch.int32, device="cuda")
 cyc = torch.zeros(4, dtype=torch.int64, device="cuda")
