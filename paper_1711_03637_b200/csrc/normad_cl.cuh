@@ -404,17 +404,19 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
             if (warp == 0) {
                 // output layer (network.py:308-314): the serial chain
                 const int l = lane < kNO ? lane : kNO - 1;
-                OutState st;
-                out_init(st, c);
+                OutD X;
+                out_init(X.o, c);
                 const double *gp = P + l;
                 uint16_t *om = OMASK;
+                X.o.Af = __dadd_rn(__dmul_rn(0.0, c.decay_slow), gp[0]);
+                X.o.Bf = __dadd_rn(__dmul_rn(0.0, c.decay_fast), gp[0]);
+                X.D0 = __dadd_rn(__dsub_rn(X.o.Af, X.o.Bf), __dmul_rn(c.inhibition, __dsub_rn(0.0, 0.0)));
                 const int ns = (skip & 1) ? 0 : N;
                 for (int s = 0; s < ns; ++s) {
-                    double ff;
-                    out_step(st, c, gp[s * kNO], s, l, &ff);
-                    if (lane == 0) om[s] = (uint16_t)st.prev;
+                    outd_step(X, c, gp[(s + 1 < N ? s + 1 : s) * kNO], s, l);
+                    if (lane == 0) om[s] = (uint16_t)X.o.prev;
                 }
-                if (lane < kNO) T.counts[(size_t)i * kNO + lane] = st.cnt;
+                if (lane < kNO) T.counts[(size_t)i * kNO + lane] = X.o.cnt;
 #ifdef SNN_NORMAD_PROFILE
                 if (clk && lane == 0) clk[12] = clock64();
 #endif

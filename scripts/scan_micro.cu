@@ -283,6 +283,7 @@ __device__ __forceinline__ bool outc_step(OutC &st, const snn_consts_t &c, doubl
     return true;
 }
 
+
 // experimental step variants (same state as OutState; extra fields below)
 struct XState {
     DistState o;
@@ -421,6 +422,20 @@ __global__ void k_scan(snn_consts_t c, const double *G, int n_img, int32_t *coun
                 }
                 t1 = clock64();
                 v = st.v; cnt = st.cnt;
+            } else if (V == 7) {
+                OutD X;
+                out_init(X.o, c);
+                // step 0's feed-forward and drive (no spikes before it: S0 = c0 = +0)
+                X.o.Af = __dadd_rn(__dmul_rn(0.0, c.decay_slow), gp[0]);
+                X.o.Bf = __dadd_rn(__dmul_rn(0.0, c.decay_fast), gp[0]);
+                X.D0 = __dadd_rn(__dsub_rn(X.o.Af, X.o.Bf), __dmul_rn(c.inhibition, __dsub_rn(0.0, 0.0)));
+                t0 = clock64();
+                for (int s = 0; s < N; ++s) {
+                    outd_step(X, c, gp[(s + 1 < N ? s + 1 : s) * kNO], s, l);
+                    if (lane == 0) om[s] = (uint16_t)X.o.prev;
+                }
+                t1 = clock64();
+                v = X.o.v; cnt = X.o.cnt;
             } else if (V == 6) {
                 OutC sc;
                 outc_init(sc, c);
@@ -758,6 +773,7 @@ extern "C" int micro_scan(const snn_consts_t *c, const double *G, int n_img, int
     case 3: k_scan<3><<<1, threads, sm>>>(*c, G, n_img, counts, cyc, om, v); break;
     case 12: k_scan<12><<<1, threads, sm>>>(*c, G, n_img, counts, cyc, om, v); break;
     case 13: k_scan<13><<<1, threads, sm>>>(*c, G, n_img, counts, cyc, om, v); break;
+    case 7: k_scan<7><<<1, threads, sm>>>(*c, G, n_img, counts, cyc, om, v); break;
     case 6: k_scan<6><<<1, threads, sm>>>(*c, G, n_img, counts, cyc, om, v); break;
     case 4: k_scan2<<<1, threads < 64 ? 64 : threads, sm>>>(*c, G, n_img, counts, cyc, om, v); break;
     default: return -1;
