@@ -425,3 +425,31 @@ def test_lateral_inhibition_never_helps_non_winners(sd, cfg, bank, toy):
     for a, b in zip(with_c, without_c):
         winner = int(np.argmax(a))
         assert all(a[l] <= b[l] for l in range(10) if l != winner)
+
+
+def test_non_finite_in_a_later_chunk(sd, cfg, bank, workloads):
+    """The abort of normad.py:122-124 when the failing image sits in a later
+    chunk, whose lists were prepared on the auxiliary stream: 100 blank
+    images (their gate stays closed: no update), then digits whose first
+    update overflows; the status names image 100 and the weights are those
+    of before it."""
+    from paper_1711_03637_b200.engine import get_engine, make_consts
+    eng = get_engine()
+    learn = sd.LearnConfig(learning_rate=1e308)
+    c = make_consts(cfg, bank, learn)
+    n_blank = 100
+    order = workloads["c2_order"][:300]
+    imgs = np.concatenate([np.zeros((n_blank, 784), dtype=np.uint8),
+                           workloads["c2_images"][order].reshape(len(order), -1)])
+    labs = np.concatenate([np.zeros(n_blank, dtype=np.uint8), workloads["c2_labels"][order].astype(np.uint8)])
+    assert int(eng.lib.snn_train_chunk(__import__("ctypes").byref(c), len(imgs))) < len(imgs)  # several chunks
+    w0 = np.full((8112, 10), np.finfo(np.float64).max)
+    d_img = torch.from_numpy(imgs.copy()).to(eng.device)
+    d_lab = torch.from_numpy(labs.copy()).to(eng.device)
+    d_w = torch.from_numpy(w0.copy()).to(eng.device)
+    _, status = eng.train(c, d_img, d_lab, d_w)
+    st = status.cpu().numpy()
+    assert st[0] == 1001 and st[1] == n_blank, st   # SNN_ENONFINITE at image 100
+    assert np.array_equal(d_w.cpu().numpy(), w0)
+    with pytest.raises(sd.NumericFailureError):
+        sd.train_epoch(imgs, labs, w0, bank, cfg, learn)
