@@ -477,24 +477,26 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
         stamp(8);
         // dW for the shard's active neurons (spikes ascending); commit with an undo log
         bool bad = false;
-        for (int a = tid; a < ((skip & 4) ? 0 : B.n_act); a += kClThreads) {
+        // five threads per active row, two outputs each
+        for (int t = tid; t < ((skip & 4) ? 0 : 5 * B.n_act); t += kClThreads) {
+            const int a = t / 5, h = (t - a * 5) * 2;
             const int row = B.act[a];
-            double acc[kNO];
+            double acc[2];
 #pragma unroll
-            for (int l = 0; l < kNO; ++l) acc[l] = 0.0;
+            for (int l = 0; l < 2; ++l) acc[l] = 0.0;
             const int e1 = B.aoff[a + 1];
             for (int e = B.aoff[a]; e < e1; ++e) {
-                const double *rr = Rloc + (int)B.nsp[e] * kNO;
+                const double *rr = Rloc + (int)B.nsp[e] * kNO + h;
 #pragma unroll
-                for (int l = 0; l < kNO; ++l) acc[l] = __dadd_rn(acc[l], rr[l]);
+                for (int l = 0; l < 2; ++l) acc[l] = __dadd_rn(acc[l], rr[l]);
             }
 #pragma unroll
-            for (int l = 0; l < kNO; ++l) {
-                const double old = Wsh[row * kNO + l];
+            for (int l = 0; l < 2; ++l) {
+                const double old = Wsh[row * kNO + h + l];
                 const double nw = __dadd_rn(old, __dmul_rn(c.learning_rate, acc[l]));
                 bad |= !isfinite(nw);
-                undo[row * kNO + l] = old;
-                Wsh[row * kNO + l] = nw;
+                undo[row * kNO + h + l] = old;
+                Wsh[row * kNO + h + l] = nw;
             }
         }
         const int any_bad = __syncthreads_or(bad);
