@@ -350,21 +350,32 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
         stamp(0);
         const ClBuf &B = s_buf[i & 1];
         // ---- G partials of this shard (ascending id within the shard)
-        for (int t = tid; t < ((skip & 8) ? 0 : N * kNO); t += kClThreads) {
-            const int s = t / kNO, l = t - s * kNO;
+        // a thread per (step, output pair): two sums, one 16-byte store
+        for (int t = tid; t < ((skip & 8) ? 0 : N * (kNO / 2)); t += kClThreads) {
+            const int s = t / (kNO / 2), l = 2 * (t - s * (kNO / 2));
             const int e1 = B.soff[s + 1];
-            double g = 0.0;
+            double g0 = 0.0, g1 = 0.0;
             int e = B.soff[s];
             for (; e + 4 <= e1; e += 4) {
                 int id[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) id[u] = B.sid[e + u];
+                double2 wv[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) g = __dadd_rn(g, Wsh[id[u] * kNO + l]);
+                for (int u = 0; u < 4; ++u) wv[u] = *reinterpret_cast<const double2 *>(Wsh + id[u] * kNO + l);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    g0 = __dadd_rn(g0, wv[u].x);
+                    g1 = __dadd_rn(g1, wv[u].y);
+                }
             }
-            for (; e < e1; ++e) g = __dadd_rn(g, Wsh[(int)B.sid[e] * kNO + l]);
-            if (push) PQ_lead[t] = g;
-            else P[t] = g;
+            for (; e < e1; ++e) {
+                const double2 wv = *reinterpret_cast<const double2 *>(Wsh + (int)B.sid[e] * kNO + l);
+                g0 = __dadd_rn(g0, wv.x);
+                g1 = __dadd_rn(g1, wv.y);
+            }
+            double2 *dst = reinterpret_cast<double2 *>((push ? PQ_lead : P) + s * kNO + l);
+            *dst = make_double2(g0, g1);
         }
         stamp(1);
         cluster.sync();  // B1: partials ready, flags of image i-1 published
