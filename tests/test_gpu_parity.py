@@ -161,6 +161,10 @@ def test_full_10k_prefix_matches(sd, cfg, bank, golden, workloads, wfix):
     got = sd.batch_counts(workloads["c3_images"], wfix["w_fix"], bank, cfg)
     assert got.shape == (10000, 10)
     assert np.array_equal(got[:200], golden["c3_counts_200"])
+    # all 10,000 against the reference's own batch_counts (oracle/gen_c3_counts.py)
+    import os
+    ref = np.load(os.path.join(os.path.dirname(__file__), "golden", "c3_counts_reference.npz"))["counts"]
+    assert np.array_equal(got, ref.astype(np.int64)), int((got != ref).any(axis=1).sum())
     # size-independent properties of the whole batch: at most one spike per
     # output per (refractory + 1) steps, and the batch equals per-image calls
     assert got.max() <= cfg.n_steps // 4 + 1
