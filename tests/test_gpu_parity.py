@@ -84,6 +84,10 @@ def test_counts_t75_canvases(sd, cfg, bank, golden, workloads, wfix):
     cfg75 = dataclasses.replace(cfg, t=0.075)
     got = np.stack([sd.run_presentation(x, wfix["w_fix"], bank, cfg75) for x in workloads["c4_images"][:100]])
     assert np.array_equal(got, golden["c4_counts_t75_100"])
+    # all 500 canvases (batched) against the reference's own batch_counts
+    import os
+    ref = np.load(os.path.join(os.path.dirname(__file__), "golden", "c3_counts_reference.npz"))["c4_counts_t75"]
+    assert np.array_equal(sd.batch_counts(workloads["c4_images"], wfix["w_fix"], bank, cfg75), ref.astype(np.int64))
 
 
 def test_counts_dt01(sd, cfg, bank, golden, workloads, wfix):
