@@ -461,3 +461,28 @@ def test_non_finite_in_a_later_chunk(sd, cfg, bank, workloads):
     assert np.array_equal(d_w.cpu().numpy(), w0)
     with pytest.raises(sd.NumericFailureError):
         sd.train_epoch(imgs, labs, w0, bank, cfg, learn)
+
+
+def test_paper_dt01_against_reference(sd, cfg, bank, workloads, wfix):
+    """The paper's dt = 0.1 ms (N = 1,000) against the
+    reference's own runs (oracle/gen_dt01.py): counts of 200 images, and 40
+    images of online NormAD from zero weights (cluster kernel with the
+    aliased sigma/R array) -- per-image counts identical, weights within 1e-12."""
+    import os
+    ref = np.load(os.path.join(os.path.dirname(__file__), "golden", "dt01_reference.npz"))
+    cfg01 = dataclasses.replace(cfg, dt=1e-4)
+    got = sd.batch_counts(workloads["c3_images"][:200], wfix["w_fix"], bank, cfg01)
+    assert np.array_equal(got, ref["c3_counts_200"].astype(np.int64))
+    from paper_1711_03637_b200.engine import get_engine, make_consts
+    eng = get_engine()
+    c = make_consts(cfg01, bank, sd.LearnConfig())
+    order = workloads["c2_order"][:40]
+    d_img = torch.from_numpy(workloads["c2_images"][order].reshape(40, -1).copy()).to(eng.device)
+    d_lab = torch.from_numpy(workloads["c2_labels"][order].astype(np.uint8)).to(eng.device)
+    d_w = torch.zeros((8112, 10), dtype=torch.float64, device=eng.device)
+    counts, status = eng.train(c, d_img, d_lab, d_w)
+    assert int(status[0]) == 0
+    assert np.array_equal(counts.cpu().numpy(), ref["train_counts_40"].astype(np.int32))
+    w = d_w.cpu().numpy()
+    rel = np.abs(w - ref["train_w_40"]).max() / np.abs(ref["train_w_40"]).max()
+    assert rel <= 1e-12, rel
