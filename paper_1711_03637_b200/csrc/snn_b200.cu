@@ -135,6 +135,7 @@ size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base, 
     w.wp = (double *)take(n * kMaxTiles * N * 8);
     w.evcap = (int64_t)cap;
     ShardWS x;
+    memset(&x, 0, sizeof(x));  // flags (push, alias, skip) are set by the caller
     x.clk = nullptr;
     x.q = (double *)take(n * N * 8);
     x.soff = (int32_t *)take(n * kCl * (N + 1) * 4);
@@ -470,6 +471,7 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
         Sb[1].clk = SW.clk;
         Sb[1].push = SW.push;
         Sb[1].alias = SW.alias;
+        Sb[1].skip = SW.skip;
         Sb[1].skip = SW.skip;
     }
     auto prepare = [&](int64_t i0, int64_t cn, int b, cudaStream_t st) -> int {
