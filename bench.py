@@ -46,6 +46,7 @@ F_TRAIN_PER_IMAGE = 162_240
 # (default filter bank): stencil = 8 chains (4 Sobel, 4 corner) with
 # 8 DMUL + 52 DFMA = 112 flop, Sobel negations are free; LIF = 12 x 5 flop.
 FLOP_PER_ACTIVE_POS_STEP = 112 + 12 * 5
+FP64_PIPE_OPS_PER_POS_STEP = 128   # k_hidden inner loop: 50 DFMA + 29 DMUL + 37 DADD + 12 DSETP (SASS)
 LAUNCHES_PER_CHUNK = 5   # per sub-batch: k_prep, k_tile_scan, k_hidden, k_gsum, k_output
 PIPE_IMAGES = 0          # snn_set_pipeline sub-batch (library default: off)
 
@@ -365,7 +366,12 @@ def run_ours(args):
                          "call_achieved_tflops": exec_flop_launch / (call_ms * 1e-3) / 1e12,
                          "dense_equiv_tflops": dense_tflops,
                          "dense_equiv_basis": "SURVEY 8(d) F_inf = 389,516 flop per image-step",
-                         "fp32_peak_tflops": f32, "active_windows_per_image": float(act.mean())},
+                         "fp32_peak_tflops": f32, "active_windows_per_image": float(act.mean()),
+                         "fp64_pipe_frac": achieved / FLOP_PER_ACTIVE_POS_STEP * FP64_PIPE_OPS_PER_POS_STEP / (f64 / 2),
+                         "fp64_pipe_basis": f"{FP64_PIPE_OPS_PER_POS_STEP} FP64-pipe instructions per active window-step "
+                                            "(50 DFMA + 29 DMUL + 37 DADD + 12 DSETP in the SASS of the inner "
+                                            "loop) against the DFMA instruction rate (peak / 2); ncu's "
+                                            "sm__pipe_fp64_cycles_active is the same quantity measured"},
             "clocks": clocks,
             "parity": {"c3_first200_counts_equal_reference": ref_prefix,
                        "c3_all10000_counts_equal_reference": ref_all},
