@@ -238,9 +238,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only overrides (SNN_BENCH_DEVICE / SNN_BENCH_BACKEND): run several
+    # ranks on one GPU over gloo to exercise the multi-rank path on a 1-GPU box
+    local = int(os.environ.get("SNN_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SNN_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
@@ -311,7 +318,7 @@ def run_ours(args):
         gold = np.load(os.path.join(ROOT, "tests", "golden", "reference_golden.npz"))["c3_counts_200"]
         ref_prefix = bool(np.array_equal(counts_dev[:200].cpu().numpy(), gold)) if counts_dev.shape[0] >= 200 else None
     ref_all = None
-    if world == 1 and counts_dev.shape[0] == N_IMAGES:  # all 10,000 vs the reference's own batch_counts
+    if rank == 0 and counts_dev.shape[0] == N_IMAGES:  # all 10,000 (gathered) vs the reference's own batch_counts
         ref10k = np.load(os.path.join(ROOT, "tests", "golden", "c3_counts_reference.npz"))["counts"]
         ref_all = bool(np.array_equal(counts_dev.cpu().numpy(), ref10k))
 

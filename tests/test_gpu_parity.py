@@ -486,3 +486,23 @@ def test_paper_dt01_against_reference(sd, cfg, bank, workloads, wfix):
     w = d_w.cpu().numpy()
     rel = np.abs(w - ref["train_w_40"]).max() / np.abs(ref["train_w_40"]).max()
     assert rel <= 1e-12, rel
+
+
+def test_bench_two_ranks_one_gpu():
+    """bench.py's multi-rank path (sharding, max over ranks, the counts
+    gather, rank-0 JSON) with two ranks sharing cuda:0 over gloo."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SNN_BENCH_BACKEND="gloo", SNN_BENCH_DEVICE="0")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29557", os.path.join(root, "bench.py"),
+                        "--gpus", "2", "--steps", "2", "--warmup", "3", "--skip-c5", "--skip-train",
+                        "--skip-latency", "--skip-cpu"], capture_output=True, text=True, env=env, cwd=root,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "dp2"
+    assert line["parity"]["c3_all10000_counts_equal_reference"] is True
