@@ -154,40 +154,62 @@ __global__ void __launch_bounds__(kThreads) k_prep(const BatchArgs A) {
 }
 
 // k_tile_scan: tile_base / win_base = exclusive prefixes of n_tiles / n_win;
-// one CTA, any n.
-__device__ __forceinline__ void block_prefix(const int32_t *in, int32_t *out, int64_t n, int *s_w, int &s_tot,
-                                             int &s_carry) {
+// one CTA, any n.  Both prefixes in one pass, 8 consecutive images per thread
+// per round (8,192 images per round): a 10k-image batch takes two rounds.
+__global__ void __launch_bounds__(1024) k_tile_scan(const BatchArgs A) {
+    constexpr int kPer = 8;
+    __shared__ int s_w[2][32];
+    __shared__ int s_carry[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_carry = 0;
+    const int64_t n = A.n_images;
+    if (tid < 2) s_carry[tid] = 0;
     __syncthreads();
-    for (int64_t base = 0; base < n; base += 1024) {
-        const int64_t i = base + tid;
-        const int x = i < n ? in[i] : 0;
-        int tot;
-        const int ex = warp_excl_scan_int(x, &tot);
-        if (lane == 0) s_w[warp] = tot;
-        __syncthreads();
-        if (warp == 0) {
-            int t2;
-            const int e2 = warp_excl_scan_int(s_w[lane], &t2);
-            s_w[lane] = e2;
-            if (lane == 0) s_tot = t2;
+    for (int64_t base = 0; base < n; base += 1024 * kPer) {
+        const int64_t i0 = base + (int64_t)tid * kPer;
+        int a[kPer], b[kPer], sa = 0, sb = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const bool in = i0 + k < n;
+            a[k] = in ? A.n_tiles[i0 + k] : 0;
+            b[k] = in ? A.n_win[i0 + k] : 0;
+            const int ta = a[k], tb = b[k];
+            a[k] = sa;  // exclusive within the thread
+            b[k] = sb;
+            sa += ta;
+            sb += tb;
+        }
+        int ta, tb;
+        const int ea = warp_excl_scan_int(sa, &ta), eb = warp_excl_scan_int(sb, &tb);
+        if (lane == 0) {
+            s_w[0][warp] = ta;
+            s_w[1][warp] = tb;
         }
         __syncthreads();
-        if (i < n) out[i] = s_carry + s_w[warp] + ex;
+        if (warp == 0) {
+            int t2, t3;
+            const int e2 = warp_excl_scan_int(s_w[0][lane], &t2), e3 = warp_excl_scan_int(s_w[1][lane], &t3);
+            s_w[0][lane] = e2 + s_carry[0];
+            s_w[1][lane] = e3 + s_carry[1];
+            __syncwarp();
+            if (lane == 0) {
+                s_carry[0] += t2;
+                s_carry[1] += t3;
+            }
+        }
         __syncthreads();
-        if (tid == 0) s_carry += s_tot;
+        const int oa = s_w[0][warp] + ea, ob = s_w[1][warp] + eb;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if (i0 + k < n) {
+                A.tile_base[i0 + k] = oa + a[k];
+                A.win_base[i0 + k] = ob + b[k];
+            }
         __syncthreads();
     }
-    if (tid == 0) out[n] = s_carry;
-    __syncthreads();
-}
-
-__global__ void __launch_bounds__(1024) k_tile_scan(const BatchArgs A) {
-    __shared__ int s_w[32];
-    __shared__ int s_tot, s_carry;
-    block_prefix(A.n_tiles, A.tile_base, A.n_images, s_w, s_tot, s_carry);
-    block_prefix(A.n_win, A.win_base, A.n_images, s_w, s_tot, s_carry);
+    if (tid == 0) {
+        A.tile_base[n] = s_carry[0];
+        A.win_base[n] = s_carry[1];
+    }
 }
 
 // ---------------------------------------------------------------------------
