@@ -94,7 +94,7 @@ __host__ __device__ inline size_t cl_buf_bytes(int N) {
 __host__ __device__ inline size_t normad_cl_smem_bytes(int N, bool push, bool alias = false) {
     return (size_t)kClRows * kNO * 8          // W shard
            + (size_t)N * kNO * 8 * (alias ? 1 : 2)  // P (G on the leader), sigma -> R
-           + (size_t)N * 8                    // q
+           + (size_t)((N + 1) & ~1) * 8       // q (padded to 16 bytes)
            + (size_t)N * 2 + 64 + 16          // OMASK, flags
            + 2 * ((cl_buf_bytes(N) + 15) & ~(size_t)15)
            + (push ? (size_t)kCl * N * kNO * 8 : 0);  // the partials of every CTA (leader)
@@ -262,7 +262,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
     double *P = Wsh + (size_t)kClRows * kNO;    // [N][10] partial G (leader: G)
     double *SR = SW.alias ? P : P + (size_t)N * kNO;  // [N][10] sigma, then R in place
     double *Q = P + (size_t)N * kNO * (SW.alias ? 1 : 2);  // [N] dt / |d_hat|
-    uint16_t *OMASK = reinterpret_cast<uint16_t *>(Q + N);
+    uint16_t *OMASK = reinterpret_cast<uint16_t *>(Q + ((N + 1) & ~1));  // keeps what follows 16-byte aligned
     int *flags = reinterpret_cast<int *>(OMASK + ((N + 7) & ~7));  // leader: per-CTA non-finite flags
     uint8_t *bufmem = reinterpret_cast<uint8_t *>(flags + 16);
     const size_t bstride = (cl_buf_bytes(N) + 15) & ~(size_t)15;

@@ -506,3 +506,23 @@ def test_bench_two_ranks_one_gpu():
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "dp2"
     assert line["parity"]["c3_all10000_counts_equal_reference"] is True
+
+
+@pytest.mark.parametrize("n_steps", [1, 7, 9, 17, 75])
+def test_short_trials_against_oracle(sd, cfg, bank, workloads, wfix, oracle, n_steps):
+    """Trials shorter than one 8-step raster chunk or not a multiple of it:
+    inference counts and a 6-image NormAD epoch against the oracle."""
+    t = n_steps * cfg.dt
+    cfgn = dataclasses.replace(cfg, t=t)
+    p = oracle.params_from_reference(cfgn, bank)
+    assert p.n_steps == n_steps
+    imgs = workloads["c3_images"][:8]
+    got = sd.batch_counts(imgs, wfix["w_fix"], bank, cfgn)
+    want = np.stack([oracle.simulate(x, wfix["w_fix"], p)["counts"] for x in imgs])
+    assert np.array_equal(got, want)
+    order = workloads["c2_order"][:6]
+    ims, labs = workloads["c2_images"][order], workloads["c2_labels"][order]
+    w, _ = sd.train_epoch(ims, labs, sd.zero_weights(), bank, cfgn, sd.LearnConfig())
+    wo, _ = oracle.train_epoch(ims, labs, np.zeros((8112, 10)), p)
+    scale = max(np.abs(wo).max(), 1e-300)
+    assert np.abs(w - wo).max() / scale <= 1e-12
