@@ -526,3 +526,63 @@ def test_short_trials_against_oracle(sd, cfg, bank, workloads, wfix, oracle, n_s
     wo, _ = oracle.train_epoch(ims, labs, np.zeros((8112, 10)), p)
     scale = max(np.abs(wo).max(), 1e-300)
     assert np.abs(w - wo).max() / scale <= 1e-12
+
+
+@pytest.mark.parametrize("variant", ["dt2ms", "bank", "rate0"])
+def test_config_variants_train_against_oracle(sd, cfg, bank, workloads, wfix, oracle, variant):
+    """Configurations off the default path, inference and a 6-image NormAD
+    epoch against the oracle: dt = 2 ms (t_ref/dt = 1.5, a non-integer
+    refractory horizon), a random non-default filter bank (the generic hidden
+    kernel inside training), and desired_rate = 0 (no desired spikes)."""
+    rng = np.random.default_rng(5)
+    b = bank
+    c_ = cfg
+    if variant == "dt2ms":
+        c_ = dataclasses.replace(cfg, dt=2e-3)
+    elif variant == "bank":
+        kernels = rng.integers(-3, 4, size=(12, 3, 3)).astype(np.float64)
+        b = sd.FilterBank(kernels=kernels, gains=rng.uniform(1e-9, 4e-9, size=12))
+    else:
+        c_ = dataclasses.replace(cfg, desired_rate=0.0)
+    p = oracle.params_from_reference(c_, b)
+    imgs = workloads["c3_images"][:6]
+    w = wfix["w_fix"]
+    got = sd.batch_counts(imgs, w, b, c_)
+    want = np.stack([oracle.simulate(x, w, p)["counts"] for x in imgs])
+    assert np.array_equal(got, want)
+    order = workloads["c2_order"][:6]
+    ims, labs = workloads["c2_images"][order], workloads["c2_labels"][order]
+    wg, _ = sd.train_epoch(ims, labs, sd.zero_weights(), b, c_, sd.LearnConfig())
+    wo, _ = oracle.train_epoch(ims, labs, np.zeros((8112, 10)), p)
+    scale = max(np.abs(wo).max(), 1e-300)
+    assert np.abs(wg - wo).max() / scale <= 1e-12
+
+
+def test_dense_images_overflow_paths(sd, cfg, bank, wfix, oracle):
+    """Dense inputs drive the paths digit images rarely reach: steps with
+    more than kStepCap hidden spikes (k_gsum's tile-by-tile slow path), shard
+    lists beyond the cluster kernel's shared-memory caps (served from global
+    memory), and all 22 tiles of an image.  Uniform noise, a white image and
+    a checkerboard, against the oracle (inference and a NormAD epoch)."""
+    rng = np.random.default_rng(11)
+    imgs = np.stack([rng.integers(0, 256, (28, 28)), np.full((28, 28), 255),
+                     (np.indices((28, 28)).sum(0) % 2) * 255, rng.integers(128, 256, (28, 28))]).astype(np.uint8)
+    # a strong all-positive bank makes whole feature maps fire in lockstep
+    bank = sd.FilterBank(kernels=np.ones((12, 3, 3)), gains=np.full(12, 3e-9))
+    p = oracle.params_from_reference(cfg, bank)
+    w = wfix["w_fix"]
+    got = sd.batch_counts(imgs, w, bank, cfg)
+    recs = [oracle.simulate(x, w, p, record=True) for x in imgs]
+    assert np.array_equal(got, np.stack([r["counts"] for r in recs]))
+    assert max(int(r["hidden"].sum(axis=1).max()) for r in recs) > 256   # the slow path ran
+    for k in range(2):
+        rec = sd.forward_pass(imgs[k], w, bank, cfg)
+        hm = np.zeros((cfg.n_steps, 8112), dtype=bool)
+        for nidx, steps in enumerate(rec.hidden_spikes):
+            hm[steps, nidx] = True
+        assert np.array_equal(hm, recs[k]["hidden"])
+    labs = np.array([3, 7, 1, 8])
+    wg, _ = sd.train_epoch(imgs, labs, sd.zero_weights(), bank, cfg, sd.LearnConfig())
+    wo, _ = oracle.train_epoch(imgs, labs, np.zeros((8112, 10)), p)
+    scale = max(np.abs(wo).max(), 1e-300)
+    assert np.abs(wg - wo).max() / scale <= 1e-12
