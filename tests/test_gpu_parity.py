@@ -528,12 +528,14 @@ def test_short_trials_against_oracle(sd, cfg, bank, workloads, wfix, oracle, n_s
     assert np.abs(w - wo).max() / scale <= 1e-12
 
 
-@pytest.mark.parametrize("variant", ["dt2ms", "bank", "rate0"])
+@pytest.mark.parametrize("variant", ["dt2ms", "bank", "rate0", "lifpos"])
 def test_config_variants_train_against_oracle(sd, cfg, bank, workloads, wfix, oracle, variant):
     """Configurations off the default path, inference and a 6-image NormAD
     epoch against the oracle: dt = 2 ms (t_ref/dt = 1.5, a non-integer
     refractory horizon), a random non-default filter bank (the generic hidden
-    kernel inside training), and desired_rate = 0 (no desired spikes)."""
+    kernel inside training), desired_rate = 0 (no desired spikes) and hidden /
+    output LIFs with positive rest and threshold (the FP64-compare variant of
+    the LIF step instead of the IEEE bit-pattern one)."""
     rng = np.random.default_rng(5)
     b = bank
     c_ = cfg
@@ -542,8 +544,11 @@ def test_config_variants_train_against_oracle(sd, cfg, bank, workloads, wfix, or
     elif variant == "bank":
         kernels = rng.integers(-3, 4, size=(12, 3, 3)).astype(np.float64)
         b = sd.FilterBank(kernels=kernels, gains=rng.uniform(1e-9, 4e-9, size=12))
-    else:
+    elif variant == "rate0":
         c_ = dataclasses.replace(cfg, desired_rate=0.0)
+    else:  # rest and threshold both positive: the FP64-compare (not bit-pattern) LIF variant
+        lif = sd.LifParams(rest_potential=30e-3, threshold=120e-3)
+        c_ = dataclasses.replace(cfg, hidden_lif=lif, output_lif=lif)
     p = oracle.params_from_reference(c_, b)
     imgs = workloads["c3_images"][:6]
     w = wfix["w_fix"]
