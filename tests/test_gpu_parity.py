@@ -591,3 +591,27 @@ def test_dense_images_overflow_paths(sd, cfg, bank, wfix, oracle):
     wo, _ = oracle.train_epoch(imgs, labs, np.zeros((8112, 10)), p)
     scale = max(np.abs(wo).max(), 1e-300)
     assert np.abs(wg - wo).max() / scale <= 1e-12
+
+
+def test_concurrent_callers(sd, cfg, bank, workloads, wfix):
+    """service.py:107 runs run_presentation from a thread pool: concurrent
+    calls (and a concurrent batch_counts / preprocess / train_epoch) give the
+    same results as sequential ones."""
+    from concurrent.futures import ThreadPoolExecutor
+    imgs = workloads["c4_images"][:48]
+    cfg75 = dataclasses.replace(cfg, t=0.075)
+    seq = np.stack([sd.run_presentation(x, wfix["w_fix"], bank, cfg75) for x in imgs])
+    order = workloads["c2_order"][:8]
+    ims, labs = workloads["c2_images"][order], workloads["c2_labels"][order]
+    w_seq, _ = sd.train_epoch(ims, labs, sd.zero_weights(), bank, cfg, sd.LearnConfig())
+    b_seq = sd.batch_counts(workloads["c3_images"][:64], wfix["w_fix"], bank, cfg)
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        fut = [ex.submit(sd.run_presentation, x, wfix["w_fix"], bank, cfg75) for x in imgs]
+        ft = ex.submit(sd.train_epoch, ims, labs, sd.zero_weights(), bank, cfg, sd.LearnConfig())
+        fb = ex.submit(sd.batch_counts, workloads["c3_images"][:64], wfix["w_fix"], bank, cfg)
+        par = np.stack([f.result() for f in fut])
+        w_par = ft.result()[0]
+        b_par = fb.result()
+    assert np.array_equal(par, seq)
+    assert np.array_equal(w_par, w_seq)
+    assert np.array_equal(b_par, b_seq)
