@@ -609,9 +609,14 @@ def test_concurrent_callers(sd, cfg, bank, workloads, wfix):
         fut = [ex.submit(sd.run_presentation, x, wfix["w_fix"], bank, cfg75) for x in imgs]
         ft = ex.submit(sd.train_epoch, ims, labs, sd.zero_weights(), bank, cfg, sd.LearnConfig())
         fb = ex.submit(sd.batch_counts, workloads["c3_images"][:64], wfix["w_fix"], bank, cfg)
+        canvas = np.zeros((60, 50), dtype=np.uint8)
+        canvas[10:40, 20:24] = 255
+        fp = [ex.submit(sd.preprocess_pipeline, canvas) for _ in range(8)]
         par = np.stack([f.result() for f in fut])
+        pre = [f.result() for f in fp]
         w_par = ft.result()[0]
         b_par = fb.result()
     assert np.array_equal(par, seq)
     assert np.array_equal(w_par, w_seq)
     assert np.array_equal(b_par, b_seq)
+    assert all(np.array_equal(x, sd.preprocess_pipeline(canvas)) for x in pre)
