@@ -193,8 +193,8 @@ class Engine:
 
     def infer_one(self, c, image: np.ndarray, w=None, check=None) -> np.ndarray:
         """One presentation through a CUDA graph captured per configuration:
-        pinned H2D of the 784-byte image, one graph launch (k_prep ..
-        k_output), D2H of the counts.  Same kernels and results as infer().
+        one graph launch holding the pinned H2D of the 784-byte image,
+        k_prep .. k_output and the D2H of the counts.  Same kernels and results as infer().
         Without `w`, the weights last set by weights() are used."""
         torch = _torch()
         d_w = self.weights(w, check) if w is not None else self._w_dev
@@ -214,19 +214,21 @@ class Engine:
                     ws.data_ptr(), ws_bytes, self.sptr)
             _native.check(self.lib.snn_infer(*args))   # first launch: lazy attributes, module load
             self.stream.synchronize()
+            img_h = torch.zeros((1, N_INPUTS), dtype=torch.uint8).pin_memory()
+            cnt_h = torch.zeros((1, N_OUTPUTS), dtype=torch.int32).pin_memory()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=self.stream):
+            with torch.cuda.graph(g, stream=self.stream):  # the copies are graph nodes too
+                img_d.copy_(img_h, non_blocking=True)
                 _native.check(self.lib.snn_infer(*args))
+                cnt_h.copy_(cnt_d, non_blocking=True)
             gr = self._graphs[key] = {"g": g, "img": img_d, "cnt": cnt_d, "ws": ws, "c": c, "o": o,
-                                      "img_h": torch.zeros((1, N_INPUTS), dtype=torch.uint8).pin_memory(),
-                                      "cnt_h": torch.zeros((1, N_OUTPUTS), dtype=torch.int32).pin_memory()}
-        gr["img_h"].numpy()[0] = image.reshape(-1)
+                                      "img_h": img_h, "cnt_h": cnt_h,
+                                      "img_np": img_h.numpy()[0], "cnt_np": cnt_h.numpy()[0]}
+        gr["img_np"][:] = image.reshape(-1)
         with torch.cuda.stream(self.stream):
-            gr["img"].copy_(gr["img_h"], non_blocking=True)
             gr["g"].replay()
-            gr["cnt_h"].copy_(gr["cnt"], non_blocking=True)
         self.stream.synchronize()
-        return gr["cnt_h"].numpy()[0].astype(np.int64)
+        return gr["cnt_np"].astype(np.int64)
 
     # ------------------------------------------------------------ training
     def train(self, c, images, labels, w):
