@@ -131,7 +131,10 @@ void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_per_sm);
 /* The hidden-layer kernel keeps the whole input table in shared memory (one
  * CTA of 20 warps per SM, no per-chunk barriers) when N <= 108 (enable = 1,
  * default), else it streams the table through a ring; enable = 0 forces the
- * ring kernel (same results). */
+ * ring kernel (same results).  With the default bank and a refractory span of
+ * 3 steps at every step (t_ref/dt = 3) the resident kernel tracks refractory
+ * neurons by the window's last three spike masks; enable = 2 keeps the
+ * per-neuron refractory horizons instead (same results; for A/B). */
 void snn_set_hidden_resident(int enable);
 
 /* snn_train runs its sequential NormAD chain on a cluster of 8 CTAs that

@@ -324,6 +324,72 @@ __device__ __forceinline__ void lif_update(double I, double &v, int &live_from, 
     }
 }
 
+// The same step when the refractory span is the same at every step (FZ frozen
+// steps after a spike, e.g. t_ref/dt = 3 -> 3): a neuron is frozen at step s
+// iff it spiked at one of the last FZ steps, so the window keeps its last FZ
+// 12-bit spike masks and `frozen` = their OR replaces the per-neuron
+// refractory horizon.  Per neuron, pa = frozen || vn >= V_T and v = (pa ||
+// vn < E_L) ? E_L : vn; the spikes are the pa bits outside `frozen`, masked
+// once per window-step.
+#ifndef SNN_FZ_INTCLAMP
+#define SNN_FZ_INTCLAMP 1
+#endif
+template <bool SGN>
+__device__ __forceinline__ void lif_update_fz(double I, double &v, unsigned frozen, const LifK &ph, unsigned &pm,
+                                              int bit) {
+    double t = __dsub_rn(v, ph.el);
+    t = __dmul_rn(ph.g, t);
+    t = __dsub_rn(I, t);
+    t = __dmul_rn(ph.beta, t);
+    const double vn = __dadd_rn(v, t);
+    if (SGN) {
+        asm("{\n\t.reg .pred pr, pa, pz;\n\t.reg .b32 q;\n\t"
+            "and.b32 q, %2, %5;\n\t"
+            "setp.ne.u32 pr, q, 0;\n\t"
+            "setp.ge.or.s64 pa, %4, %6, pr;\n\t"
+#if SNN_FZ_INTCLAMP
+            "setp.gt.or.u64 pz, %4, %8, pa;\n\t"
+#else
+            "setp.lt.or.f64 pz, %3, %7, pa;\n\t"
+#endif
+            "selp.f64 %0, %7, %3, pz;\n\t"
+            "@pa or.b32 %1, %1, %5;\n\t}"
+            : "=d"(v), "+r"(pm)
+            : "r"(frozen), "d"(vn), "l"(__double_as_longlong(vn)), "r"(1u << bit), "l"(ph.vt_bits), "d"(ph.el),
+              "l"(ph.el_bits));
+    } else {
+        asm("{\n\t.reg .pred pr, pa, pz;\n\t.reg .b32 q;\n\t"
+            "and.b32 q, %2, %4;\n\t"
+            "setp.ne.u32 pr, q, 0;\n\t"
+            "setp.ge.or.f64 pa, %3, %5, pr;\n\t"
+            "setp.lt.or.f64 pz, %3, %6, pa;\n\t"
+            "selp.f64 %0, %6, %3, pz;\n\t"
+            "@pa or.b32 %1, %1, %4;\n\t}"
+            : "=d"(v), "+r"(pm)
+            : "r"(frozen), "d"(vn), "r"(1u << bit), "d"(ph.vt), "d"(ph.el));
+    }
+}
+
+template <bool SGN>
+__device__ __forceinline__ unsigned hidden_step_def_fz(const LifK &ph, const double (&x)[9], double (&v)[kNF],
+                                                       unsigned frozen) {
+    unsigned pm = 0;
+    const double e0 = def_current<0>(x), e1 = def_current<1>(x), e2 = def_current<2>(x), e3 = def_current<3>(x);
+    lif_update_fz<SGN>(e0, v[0], frozen, ph, pm, 0);
+    lif_update_fz<SGN>(e1, v[1], frozen, ph, pm, 1);
+    lif_update_fz<SGN>(e2, v[2], frozen, ph, pm, 2);
+    lif_update_fz<SGN>(e3, v[3], frozen, ph, pm, 3);
+    lif_update_fz<SGN>(-e0, v[4], frozen, ph, pm, 4);
+    lif_update_fz<SGN>(-e1, v[5], frozen, ph, pm, 5);
+    lif_update_fz<SGN>(-e2, v[6], frozen, ph, pm, 6);
+    lif_update_fz<SGN>(-e3, v[7], frozen, ph, pm, 7);
+    lif_update_fz<SGN>(def_current<8>(x), v[8], frozen, ph, pm, 8);
+    lif_update_fz<SGN>(def_current<9>(x), v[9], frozen, ph, pm, 9);
+    lif_update_fz<SGN>(def_current<10>(x), v[10], frozen, ph, pm, 10);
+    lif_update_fz<SGN>(def_current<11>(x), v[11], frozen, ph, pm, 11);
+    return pm & ~frozen;
+}
+
 // All 12 features of one lane with the default bank: 4 Sobel currents, their
 // exact negations (fma(x,-w,-a) == -fma(x,w,a) under round-to-nearest-even),
 // and 4 corner currents -- 60 FMAs instead of 108.
@@ -428,9 +494,12 @@ __device__ __forceinline__ void item_setup(const BatchArgs &A, int item, int tot
 
 // The steps of one chunk for one live item (tab = the chunk's [8][256] table
 // rows in shared memory); stores the chunk's raster bytes.
-template <bool TRACE, bool DEF, bool SGN>
+// FZ > 0 (default bank, constant refractory span of FZ steps): live_from[0 ..
+// FZ-1] hold the window's last FZ spike masks instead of refractory horizons.
+template <bool TRACE, bool DEF, bool SGN, int FZ = 0>
 __device__ __forceinline__ void item_chunk(const BatchArgs &A, const LifK &ph, const ItemState &it, const double *tab,
                                            int ch, double (&v)[kNF], int (&live_from)[kNF]) {
+    static_assert(FZ == 0 || (DEF && !TRACE && FZ <= kNF), "FZ: default bank, no traces");
     const int N = A.c.n_steps;
     const double refr = A.c.lif_hid.refr;
     const int s0 = ch * kChunk;
@@ -443,11 +512,18 @@ __device__ __forceinline__ void item_chunk(const BatchArgs &A, const LifK &ph, c
         double x[9];
 #pragma unroll
         for (int k = 0; k < 9; ++k) x[k] = T[(it.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu];
-        const int relive = next_live_step(s, refr);
         unsigned m;
-        if (DEF) m = hidden_step_def<SGN>(ph, x, v, live_from, s, relive);
-        else m = it.half ? hidden_step<1, SGN>(A, ph, x, v, live_from, s, relive)
-                         : hidden_step<0, SGN>(A, ph, x, v, live_from, s, relive);
+        if (FZ) {
+            unsigned frozen = 0;
+#pragma unroll
+            for (int q = 0; q < FZ; ++q) frozen |= (unsigned)live_from[q];
+            m = hidden_step_def_fz<SGN>(ph, x, v, frozen);
+#pragma unroll
+            for (int q = FZ - 1; q > 0; --q) live_from[q] = live_from[q - 1];
+            live_from[0] = (int)m;
+        } else if (DEF) m = hidden_step_def<SGN>(ph, x, v, live_from, s, next_live_step(s, refr));
+        else m = it.half ? hidden_step<1, SGN>(A, ph, x, v, live_from, s, next_live_step(s, refr))
+                         : hidden_step<0, SGN>(A, ph, x, v, live_from, s, next_live_step(s, refr));
         if (TRACE && it.on && A.out.v_hid) {
             double *dst = A.out.v_hid + ((size_t)it.img * N + s) * kNH + it.pos * kNF + it.half * kHalf;
 #pragma unroll
@@ -523,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_hidden(const BatchArgs A) {
 constexpr int kResWarps = 20;
 constexpr int kResMaxSteps = 108;  // 108 * 2 KB = 216 KB of table
 
-template <bool TRACE, bool DEF, bool SGN>
+template <bool TRACE, bool DEF, bool SGN, int FZ = 0>
 __global__ void __launch_bounds__(kResWarps * 32, 1) k_hidden_res(const BatchArgs A) {
     extern __shared__ __align__(128) double r_tab[];
     __shared__ uint64_t r_full;
@@ -557,7 +633,7 @@ __global__ void __launch_bounds__(kResWarps * 32, 1) k_hidden_res(const BatchArg
             live_from[f] = 0;
         }
         for (int ch = 0; ch < nchunks; ++ch)
-            item_chunk<TRACE, DEF, SGN>(A, ph, it, r_tab + (size_t)ch * kChunk * 256, ch, v, live_from);
+            item_chunk<TRACE, DEF, SGN, FZ>(A, ph, it, r_tab + (size_t)ch * kChunk * 256, ch, v, live_from);
     }
 }
 

@@ -174,6 +174,39 @@ long long *g_phase_clk = nullptr;  // snn_normad_phase_clocks
 int g_normad_skip = 0;             // snn_normad_skip (profiling only)
 int64_t g_pipe_images = 0;
 
+// Frozen steps after a hidden spike, next_live_step(s) - s - 1 (the same fp64
+// expression as the kernels), if it is the same for every step of the trial;
+// else -1.
+int refr_span(const snn_consts_t &c) {
+    int k = -1;
+    for (int s = 0; s < c.n_steps; ++s) {
+        const int d = (int)std::floor((double)s + c.lif_hid.refr) - s;
+        if (s == 0) k = d;
+        else if (d != k) return -1;
+    }
+    return k;
+}
+#ifndef SNN_HID_FZ
+#define SNN_HID_FZ 1
+#endif
+int g_hid_fz = SNN_HID_FZ;  // -DSNN_HID_FZ=0: never the frozen-mask variant (A/B builds)
+
+template <bool TRACE, bool DEF, bool SGN, int FZ>
+int launch_hidden_res(const BatchArgs &A, cudaStream_t st) {
+    static bool attr = false;
+    const size_t smem = (size_t)A.c.n_steps * 256 * 8;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_hidden_res<TRACE, DEF, SGN, FZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(kResMaxSteps * 256 * 8)) != cudaSuccess)
+            return cuda_check("cudaFuncSetAttribute(k_hidden_res)");
+        attr = true;
+    }
+    const int64_t max_items = (int64_t)A.items_per_tile * A.n_images * kMaxTiles;
+    const unsigned grid = (unsigned)std::min<int64_t>(sm_count(), max_items);
+    k_hidden_res<TRACE, DEF, SGN, FZ><<<grid, kResWarps * 32, smem, st>>>(A);
+    return SNN_OK;
+}
+
 // prep -> tile scan -> hidden (persistent): the hidden raster of A's images
 template <bool TRACE, bool DEF, bool SGN>
 int launch_hidden(const BatchArgs &A, cudaStream_t st) {
@@ -193,17 +226,13 @@ int launch_hidden(const BatchArgs &A, cudaStream_t st) {
     if ((rc = cuda_check("k_tile_scan"))) return rc;
     if (g_ev_before) cudaEventRecord(g_ev_before, st);
     if (g_hid_res && A.c.n_steps <= kResMaxSteps) {  // table resident in shared memory
-        static bool attr = false;
-        const size_t smem = (size_t)A.c.n_steps * 256 * 8;
-        if (!attr) {
-            if (cudaFuncSetAttribute(k_hidden_res<TRACE, DEF, SGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(kResMaxSteps * 256 * 8)) != cudaSuccess)
-                return cuda_check("cudaFuncSetAttribute(k_hidden_res)");
-            attr = true;
+        if constexpr (DEF && !TRACE) {
+            if (g_hid_fz && refr_span(A.c) == 3) rc = launch_hidden_res<TRACE, DEF, SGN, 3>(A, st);
+            else rc = launch_hidden_res<TRACE, DEF, SGN, 0>(A, st);
+        } else {
+            rc = launch_hidden_res<TRACE, DEF, SGN, 0>(A, st);
         }
-        const int64_t max_items = (int64_t)A.items_per_tile * A.n_images * kMaxTiles;
-        const unsigned grid = (unsigned)std::min<int64_t>(sm_count(), max_items);
-        k_hidden_res<TRACE, DEF, SGN><<<grid, kResWarps * 32, smem, st>>>(A);
+        if (rc) return rc;
     } else {
         const int64_t max_groups = (2 * A.n_images * kMaxTiles + kWPC - 1) / kWPC;
         const unsigned grid = (unsigned)std::min<int64_t>((int64_t)per_sm * sm_count(), max_groups);
@@ -393,7 +422,10 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
 
 extern "C" void snn_set_normad_cluster(int enable) { g_normad_cluster = enable; }
 
-extern "C" void snn_set_hidden_resident(int enable) { g_hid_res = enable; }
+extern "C" void snn_set_hidden_resident(int enable) {
+    g_hid_res = enable != 0;
+    g_hid_fz = enable == 2 ? 0 : SNN_HID_FZ;
+}
 
 extern "C" void snn_normad_phase_clocks(long long *d_clk) { g_phase_clk = d_clk; }
 

@@ -367,6 +367,7 @@ def test_hidden_kernel_variants_identical(sd, cfg, bank, workloads, wfix):
     """The table-resident and the ring-streamed hidden-layer kernels give the
     same bits (snn_set_hidden_resident), and so does the one-CTA NormAD kernel
     vs the cluster kernel (snn_set_normad_cluster)."""
+    from paper_1711_03637_b200.api import decode_hidden
     from paper_1711_03637_b200.engine import get_engine, make_consts
     eng = get_engine()
     c = make_consts(cfg, bank)
@@ -389,6 +390,24 @@ def test_hidden_kernel_variants_identical(sd, cfg, bank, workloads, wfix):
     finally:
         eng.lib.snn_set_pipeline(0, 0)
     assert np.array_equal(piped, outs[0]["counts"])
+    # the frozen-mask resident kernel (default config), the horizon-based one
+    # and the ring kernel: same hidden raster and counts
+    imgs = torch.from_numpy(workloads["c3_images"][:300].reshape(300, -1).copy()).to(eng.device)
+    rast = []
+    for res in (1, 2, 0):
+        eng.lib.snn_set_hidden_resident(res)
+        try:
+            o = eng.infer(c, imgs, w, raster=True)
+            h = {k: o[k].cpu().numpy() for k in ("counts", "raster", "out_raster", "tile_base", "tile_pos", "n_tiles")}
+            h["hidden"] = np.stack([decode_hidden(h["raster"], int(h["tile_base"][i]), h["tile_pos"][i],
+                                                  int(h["n_tiles"][i]), c.n_steps) for i in range(0, 300, 7)])
+            rast.append(h)
+        finally:
+            eng.lib.snn_set_hidden_resident(1)
+    assert rast[0]["hidden"].any()
+    for r in rast[1:]:
+        for k in ("counts", "out_raster", "hidden"):
+            assert np.array_equal(rast[0][k], r[k]), k
     learn = sd.LearnConfig()
     order = workloads["c2_order"][:40]
     ims, labs = workloads["c2_images"][order], workloads["c2_labels"][order]
