@@ -46,7 +46,7 @@ F_TRAIN_PER_IMAGE = 162_240
 # (default filter bank): stencil = 8 chains (4 Sobel, 4 corner) with
 # 8 DMUL + 52 DFMA = 112 flop, Sobel negations are free; LIF = 12 x 5 flop.
 FLOP_PER_ACTIVE_POS_STEP = 112 + 12 * 5
-FP64_PIPE_OPS_PER_POS_STEP = 115   # k_hidden_res<FZ=3> inner loop: 50 DFMA + 29 DMUL + 36 DADD (SASS)
+FP64_PIPE_OPS_PER_POS_STEP = 121   # k_hidden_res<FZ=3> inner loop: 50 DFMA + 29 DMUL + 36 DADD + 6 DSETP (SASS)
 LAUNCHES_PER_CHUNK = 5   # per sub-batch: k_prep, k_tile_scan, k_hidden, k_gsum, k_output
 PIPE_IMAGES = 0          # snn_set_pipeline sub-batch (library default: off)
 
@@ -376,7 +376,7 @@ def run_ours(args):
                          "fp32_peak_tflops": f32, "active_windows_per_image": float(act.mean()),
                          "fp64_pipe_frac": achieved / FLOP_PER_ACTIVE_POS_STEP * FP64_PIPE_OPS_PER_POS_STEP / (f64 / 2),
                          "fp64_pipe_basis": f"{FP64_PIPE_OPS_PER_POS_STEP} FP64-pipe instructions per active window-step "
-                                            "(50 DFMA + 29 DMUL + 36 DADD in the SASS of the inner "
+                                            "(50 DFMA + 29 DMUL + 36 DADD + 6 DSETP in the SASS of the inner "
                                             "loop) against the DFMA instruction rate (peak / 2); ncu's "
                                             "sm__pipe_fp64_cycles_active is the same quantity measured"},
             "clocks": clocks,
