@@ -547,14 +547,17 @@ def test_short_trials_against_oracle(sd, cfg, bank, workloads, wfix, oracle, n_s
     assert np.abs(w - wo).max() / scale <= 1e-12
 
 
-@pytest.mark.parametrize("variant", ["dt2ms", "bank", "rate0", "lifpos"])
+@pytest.mark.parametrize("variant", ["dt2ms", "bank", "rate0", "lifpos", "tref35", "tref2"])
 def test_config_variants_train_against_oracle(sd, cfg, bank, workloads, wfix, oracle, variant):
     """Configurations off the default path, inference and a 6-image NormAD
     epoch against the oracle: dt = 2 ms (t_ref/dt = 1.5, a non-integer
     refractory horizon), a random non-default filter bank (the generic hidden
     kernel inside training), desired_rate = 0 (no desired spikes) and hidden /
     output LIFs with positive rest and threshold (the FP64-compare variant of
-    the LIF step instead of the IEEE bit-pattern one)."""
+    the LIF step instead of the IEEE bit-pattern one), a hidden refractory
+    period of 3.5 ms (t_ref/dt = 3.5: still 3 frozen steps, so the frozen-mask
+    hidden step with a non-integer horizon) and of 2 ms (2 frozen steps: the
+    per-neuron horizons)."""
     rng = np.random.default_rng(5)
     b = bank
     c_ = cfg
@@ -565,6 +568,9 @@ def test_config_variants_train_against_oracle(sd, cfg, bank, workloads, wfix, or
         b = sd.FilterBank(kernels=kernels, gains=rng.uniform(1e-9, 4e-9, size=12))
     elif variant == "rate0":
         c_ = dataclasses.replace(cfg, desired_rate=0.0)
+    elif variant in ("tref35", "tref2"):
+        lif = dataclasses.replace(cfg.hidden_lif, refractory=3.5e-3 if variant == "tref35" else 2e-3)
+        c_ = dataclasses.replace(cfg, hidden_lif=lif)
     else:  # rest and threshold both positive: the FP64-compare (not bit-pattern) LIF variant
         lif = sd.LifParams(rest_potential=30e-3, threshold=120e-3)
         c_ = dataclasses.replace(cfg, hidden_lif=lif, output_lif=lif)
