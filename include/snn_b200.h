@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SNN_ABI_VERSION 1
+#define SNN_ABI_VERSION 2
 
 #define SNN_IMAGE_SIDE 28
 #define SNN_N_PIXELS 784
@@ -95,6 +95,14 @@ typedef struct snn_infer_out {
     double *v_out;       /* [n][N][10] output membrane after each step */
     double *v_hid;       /* [n][N][8112] hidden membrane after each step (only
                             neurons of active windows are written) */
+    int32_t *near_ties;  /* [n] output-layer steps whose threshold decision could
+                            differ from the reference's: the output neuron is live
+                            and |v - V_T| is within a rigorous bound of the
+                            difference between the reference's c_hidden @ W
+                            (dgemv, network.py:311) and this library's
+                            event-driven sum, propagated through the LIF update
+                            (DESIGN.md section 6.1).  0 on an image means its
+                            output spikes are provably the reference's. */
 } snn_infer_out_t;
 
 int snn_abi_version(void);
@@ -119,6 +127,11 @@ int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t n_images,
  * kernel (k_hidden) and `after` just after it, so a caller can time that
  * kernel alone with cudaEventElapsedTime.  Pass NULLs to disable. */
 void snn_profile_events(void *before, void *after);
+
+/* The tuning and profiling knobs below (snn_set_*, snn_normad_*) apply to the
+ * calling thread's CURRENT CUDA device (cudaSetDevice): one process can drive
+ * several GPUs with independent settings.  Function attributes and occupancy
+ * are likewise cached per device. */
 
 /* Tuning of snn_infer: calls with more than images_per_subbatch images (and
  * no caller-visible raster) are pipelined in sub-batches -- the hidden layer

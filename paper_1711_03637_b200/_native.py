@@ -12,6 +12,8 @@ import os
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsnn_b200.so")
 
 
+ABI_VERSION = 2   # SNN_ABI_VERSION of include/snn_b200.h
+
 SNN_OK = 0
 SNN_ENOMEM = 12
 SNN_EINVAL = 22
@@ -58,7 +60,8 @@ class ConstsC(ctypes.Structure):
 
 class InferOutC(ctypes.Structure):
     _fields_ = [(name, _vp) for name in
-                ("counts", "raster", "tile_pos", "n_tiles", "tile_base", "out_raster", "ff", "v_out", "v_hid")]
+                ("counts", "raster", "tile_pos", "n_tiles", "tile_base", "out_raster", "ff", "v_out", "v_hid",
+                 "near_ties")]
 
 
 # (name, restype, argtypes) -- one row per declaration in include/snn_b200.h
@@ -101,7 +104,7 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.snn_abi_version() != 1:
+    if lib.snn_abi_version() != ABI_VERSION:
         raise ImportError("libsnn_b200.so ABI version mismatch")
     _LIB = lib
     return lib

@@ -63,7 +63,8 @@ struct InferWS {
     uint16_t *tile_pos;
     int32_t *n_tiles, *tile_base, *n_win, *win_base;
     uint8_t *raster;
-    double *g;  // [n][N][10] G rows (k_gsum -> k_output)
+    double *g;     // [n][N][10] G rows (k_gsum -> k_output)
+    double *gabs;  // [n][N][10] sum of |W| rows (near-tie accounting only)
 };
 
 size_t infer_ws_layout(const snn_consts_t *c, int64_t n, char *base, InferWS *w) {
@@ -81,6 +82,7 @@ size_t infer_ws_layout(const snn_consts_t *c, int64_t n, char *base, InferWS *w)
     x.win_base = (int32_t *)take((size_t)(n + 1 + kMaxSub) * 4);
     x.raster = (uint8_t *)take(raster_bytes(c, n));
     x.g = (double *)take((size_t)n * c->n_steps * kNO * 8);
+    x.gabs = (double *)take((size_t)n * c->n_steps * kNO * 8);
 
     if (w) *w = x;
     return off;
@@ -155,24 +157,45 @@ size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base, 
 
 cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;  // snn_profile_events
 
-int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
+// Per-device state: function attributes, occupancy and SM counts are
+// properties of a device context, and the tuning knobs (snn_set_*) apply to
+// the calling thread's current device, so one process may drive several
+// B200s (one Engine per device) with independent settings.
+constexpr int kMaxDev = 64;
+
+int cur_dev() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) dev = 0;
+    return dev;
 }
 
-// k_hidden CTAs per SM (0 = occupancy limit); snn_set_pipeline
-int g_hid_ctas = 0;
-int g_hid_res = 1;  // snn_set_hidden_resident
-int g_normad_cluster = 1;  // snn_set_normad_cluster
-long long *g_phase_clk = nullptr;  // snn_normad_phase_clocks
-int g_normad_skip = 0;             // snn_normad_skip (profiling only)
-int64_t g_pipe_images = 0;
+int g_sms[kMaxDev] = {};
+
+int sm_count() {
+    const int dev = cur_dev();
+    if (!g_sms[dev]) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        g_sms[dev] = sms > 0 ? sms : 148;
+    }
+    return g_sms[dev];
+}
+
+#ifndef SNN_HID_FZ
+#define SNN_HID_FZ 1
+#endif
+struct Knobs {
+    int hid_ctas = 0;                  // k_hidden CTAs per SM (0 = occupancy limit); snn_set_pipeline
+    int hid_res = 1;                   // snn_set_hidden_resident
+    int hid_fz = SNN_HID_FZ;           // -DSNN_HID_FZ=0: never the frozen-mask variant (A/B builds)
+    int normad_cluster = 1;            // snn_set_normad_cluster
+    long long *phase_clk = nullptr;    // snn_normad_phase_clocks
+    int normad_skip = 0;               // snn_normad_skip (profiling only)
+    int64_t pipe_images = 0;           // snn_set_pipeline
+};
+Knobs g_knobs[kMaxDev];
+
+Knobs &knobs() { return g_knobs[cur_dev()]; }
 
 // Frozen steps after a hidden spike, next_live_step(s) - s - 1 (the same fp64
 // expression as the kernels), if it is the same for every step of the trial;
@@ -186,20 +209,16 @@ int refr_span(const snn_consts_t &c) {
     }
     return k;
 }
-#ifndef SNN_HID_FZ
-#define SNN_HID_FZ 1
-#endif
-int g_hid_fz = SNN_HID_FZ;  // -DSNN_HID_FZ=0: never the frozen-mask variant (A/B builds)
-
 template <bool TRACE, bool DEF, bool SGN, int FZ>
 int launch_hidden_res(const BatchArgs &A, cudaStream_t st) {
-    static bool attr = false;
+    static bool attr[kMaxDev] = {};  // per device context (idempotent if two threads race)
     const size_t smem = (size_t)A.c.n_steps * 256 * 8;
-    if (!attr) {
+    const int dev = cur_dev();
+    if (!attr[dev]) {
         if (cudaFuncSetAttribute(k_hidden_res<TRACE, DEF, SGN, FZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(kResMaxSteps * 256 * 8)) != cudaSuccess)
             return cuda_check("cudaFuncSetAttribute(k_hidden_res)");
-        attr = true;
+        attr[dev] = true;
     }
     const int64_t max_items = (int64_t)A.items_per_tile * A.n_images * kMaxTiles;
     const unsigned grid = (unsigned)std::min<int64_t>(sm_count(), max_items);
@@ -210,14 +229,18 @@ int launch_hidden_res(const BatchArgs &A, cudaStream_t st) {
 // prep -> tile scan -> hidden (persistent): the hidden raster of A's images
 template <bool TRACE, bool DEF, bool SGN>
 int launch_hidden(const BatchArgs &A, cudaStream_t st) {
-    static int hid_blocks = 0;
+    static int hid_blocks_dev[kMaxDev] = {};
+    const Knobs &K = knobs();
+    int &hid_blocks = hid_blocks_dev[cur_dev()];
     if (!hid_blocks) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hid_blocks, k_hidden<TRACE, DEF, SGN>, kThreads, 0) !=
+        int b = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_hidden<TRACE, DEF, SGN>, kThreads, 0) !=
                 cudaSuccess ||
-            hid_blocks <= 0)
-            hid_blocks = 4;
+            b <= 0)
+            b = 4;
+        hid_blocks = b;
     }
-    const int per_sm = g_hid_ctas > 0 ? std::min(g_hid_ctas, hid_blocks) : hid_blocks;
+    const int per_sm = K.hid_ctas > 0 ? std::min(K.hid_ctas, hid_blocks) : hid_blocks;
     int rc;
     const unsigned n = (unsigned)A.n_images;
     k_prep<<<n, kThreads, 0, st>>>(A);
@@ -225,9 +248,9 @@ int launch_hidden(const BatchArgs &A, cudaStream_t st) {
     k_tile_scan<<<1, 1024, 0, st>>>(A);
     if ((rc = cuda_check("k_tile_scan"))) return rc;
     if (g_ev_before) cudaEventRecord(g_ev_before, st);
-    if (g_hid_res && A.c.n_steps <= kResMaxSteps) {  // table resident in shared memory
+    if (K.hid_res && A.c.n_steps <= kResMaxSteps) {  // table resident in shared memory
         if constexpr (DEF && !TRACE) {
-            if (g_hid_fz && refr_span(A.c) == 3) rc = launch_hidden_res<TRACE, DEF, SGN, 3>(A, st);
+            if (K.hid_fz && refr_span(A.c) == 3) rc = launch_hidden_res<TRACE, DEF, SGN, 3>(A, st);
             else rc = launch_hidden_res<TRACE, DEF, SGN, 0>(A, st);
         } else {
             rc = launch_hidden_res<TRACE, DEF, SGN, 0>(A, st);
@@ -243,14 +266,19 @@ int launch_hidden(const BatchArgs &A, cudaStream_t st) {
     return SNN_OK;
 }
 
-// G rows, then the output layer
+// G rows, then the output layer.  With near_ties requested, also the |W|
+// sums (second half of the G buffer, see InferWS) and the tie bound.
 int launch_contract(const BatchArgs &A, double *g, cudaStream_t st) {
     int rc;
     const int64_t n = A.n_images;
     const int64_t tasks = n * n_chunks(A.c.n_steps);
-    k_gsum<<<(unsigned)((tasks + kGWarps - 1) / kGWarps), kGWarps * 32, 0, st>>>(A, g);
+    const unsigned gg = (unsigned)((tasks + kGWarps - 1) / kGWarps), og = (unsigned)((n + kOutWarps2 - 1) / kOutWarps2);
+    double *gabs = A.out.near_ties ? A.gabs : nullptr;
+    if (gabs) k_gsum<true><<<gg, kGWarps * 32, 0, st>>>(A, g, gabs);
+    else k_gsum<false><<<gg, kGWarps * 32, 0, st>>>(A, g, nullptr);
     if ((rc = cuda_check("k_gsum"))) return rc;
-    k_output<<<(unsigned)((n + kOutWarps2 - 1) / kOutWarps2), kOutWarps2 * 32, 0, st>>>(A, g);
+    if (gabs) k_output<true><<<og, kOutWarps2 * 32, 0, st>>>(A, g, gabs);
+    else k_output<false><<<og, kOutWarps2 * 32, 0, st>>>(A, g, nullptr);
     return cuda_check("k_output");
 }
 
@@ -379,21 +407,23 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
     A.n_win = w.n_win;
     A.win_base = w.win_base;
     A.raster = out->raster ? out->raster : w.raster;
+    A.gabs = w.gabs;
 
     A.out = *out;
     const bool def = is_default_bank(*c);
     A.items_per_tile = def ? 1 : 2;
     if (out->v_hid) return def ? launch_batch<true, true, false>(A, w.g, s) : launch_batch<true, false, false>(A, w.g, s);
-    // Pipelined: sub-batches of g_pipe_images; the hidden layer of sub-batch
+    // Pipelined: sub-batches of pipe_images; the hidden layer of sub-batch
     // b+1 (main stream) runs while the contraction + output layer of sub-batch
     // b run on an auxiliary stream, and each sub-batch's raster is still in L2
     // when it is read.  Only when no caller-visible raster is requested (that
     // one is indexed by a single tile_base).
     const bool caller_raster = out->raster || out->tile_pos || out->n_tiles || out->tile_base;
-    Pipe *pp = (g_pipe_images > 0 && !caller_raster && n > g_pipe_images) ? pipe_for_device() : nullptr;
+    const int64_t pipe_images = knobs().pipe_images;
+    Pipe *pp = (pipe_images > 0 && !caller_raster && n > pipe_images) ? pipe_for_device() : nullptr;
     if (!pp) return def ? launch_fast<true>(A, w.g, s) : launch_fast<false>(A, w.g, s);
     std::lock_guard<std::mutex> lk(g_pipe_mu);
-    const int64_t per = std::max<int64_t>(g_pipe_images, (n + kMaxSub - 1) / kMaxSub);
+    const int64_t per = std::max<int64_t>(pipe_images, (n + kMaxSub - 1) / kMaxSub);
     const int N = c->n_steps, nch = n_chunks(N);
     int b = 0;
     for (int64_t i0 = 0; i0 < n; i0 += per, ++b) {
@@ -410,6 +440,8 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
         if (out->out_raster) B.out.out_raster = out->out_raster + i0 * N;
         if (out->ff) B.out.ff = out->ff + i0 * N * kNO;
         if (out->v_out) B.out.v_out = out->v_out + i0 * N * kNO;
+        if (out->near_ties) B.out.near_ties = out->near_ties + i0;
+        B.gabs = w.gabs + (size_t)i0 * N * kNO;
         if ((rc = def ? launch_hidden_fast<true>(B, s) : launch_hidden_fast<false>(B, s))) return rc;
         cudaEventRecord(pp->ev[b], s);
         cudaStreamWaitEvent(pp->aux, pp->ev[b], 0);
@@ -420,20 +452,22 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
     return cuda_check("snn_infer pipeline");
 }
 
-extern "C" void snn_set_normad_cluster(int enable) { g_normad_cluster = enable; }
+extern "C" void snn_set_normad_cluster(int enable) { knobs().normad_cluster = enable; }
 
 extern "C" void snn_set_hidden_resident(int enable) {
-    g_hid_res = enable != 0;
-    g_hid_fz = enable == 2 ? 0 : SNN_HID_FZ;
+    Knobs &K = knobs();
+    K.hid_res = enable != 0;
+    K.hid_fz = enable == 2 ? 0 : SNN_HID_FZ;
 }
 
-extern "C" void snn_normad_phase_clocks(long long *d_clk) { g_phase_clk = d_clk; }
+extern "C" void snn_normad_phase_clocks(long long *d_clk) { knobs().phase_clk = d_clk; }
 
-extern "C" void snn_normad_skip(int mask) { g_normad_skip = mask; }
+extern "C" void snn_normad_skip(int mask) { knobs().normad_skip = mask; }
 
 extern "C" void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_per_sm) {
-    g_pipe_images = images_per_subbatch;
-    g_hid_ctas = hidden_ctas_per_sm;
+    Knobs &K = knobs();
+    K.pipe_images = images_per_subbatch;
+    K.hid_ctas = hidden_ctas_per_sm;
 }
 
 extern "C" int64_t snn_train_chunk(const snn_consts_t *c, int64_t n) {
@@ -462,11 +496,12 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     if (((uintptr_t)d_images & 15) != 0) return set_error(SNN_EINVAL, "images must be 16-byte aligned");
     if (c->n_steps > 65535) return set_error(SNN_EINVAL, "training supports n_steps <= 65535");
     // the W-resident cluster kernel when its shared memory fits, else the one-CTA kernel
-    const bool cl_push = g_normad_cluster == 1 && normad_cl_smem_bytes(c->n_steps, true) <= 227 * 1024;
+    const Knobs &K = knobs();
+    const bool cl_push = K.normad_cluster == 1 && normad_cl_smem_bytes(c->n_steps, true) <= 227 * 1024;
     // long trials: sigma/R reuse the G array, so the cluster kernel fits up to N ~ 1,300
     const bool cl_alias = !cl_push && normad_cl_smem_bytes(c->n_steps, false) > 227 * 1024;
     const size_t cl_smem = normad_cl_smem_bytes(c->n_steps, cl_push, cl_alias);
-    const bool use_cl = g_normad_cluster && cl_smem <= 227 * 1024;
+    const bool use_cl = K.normad_cluster && cl_smem <= 227 * 1024;
     const NormadCaps caps = normad_caps(c);
     const size_t smem = normad_smem_bytes(c->n_steps, caps);
     if (!use_cl && smem > 220 * 1024) return set_error(SNN_EINVAL, "n_steps too large for the sequential NormAD CTA");
@@ -475,10 +510,10 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     memset(&T, 0, sizeof(T));
     ShardWS SW;
     const size_t need = train_ws(c, chunk, &T.ws, (char *)d_ws, &SW);
-    SW.clk = g_phase_clk;
+    SW.clk = K.phase_clk;
     SW.push = cl_push ? 1 : 0;
     SW.alias = cl_alias ? 1 : 0;
-    SW.skip = g_normad_skip;
+    SW.skip = K.normad_skip;
     if (!d_ws || ws_bytes < need) return set_error(SNN_ENOMEM, "workspace too small");
     if (use_cl) {
         if (cudaFuncSetAttribute(k_normad_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem) != cudaSuccess)

@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import math
 import threading
+from collections import OrderedDict
 
 import numpy as np
 
@@ -67,6 +68,10 @@ def table_key(c: _native.ConstsC):
     return (c.n_steps, c.dt, c.i0, c.ip, li.g, li.el, li.vt, li.beta, li.refr, c.decay_slow, c.decay_fast)
 
 
+MAX_TABLES = 8
+MAX_GRAPHS = 16
+
+
 class Engine:
     def __init__(self, device=None):
         torch = _torch()
@@ -77,11 +82,14 @@ class Engine:
         with torch.cuda.device(self.device):
             self.stream = torch.cuda.Stream(self.device)
         self.lock = threading.RLock()
-        self._tables: dict = {}
+        self._tables: OrderedDict = OrderedDict()   # LRU, MAX_TABLES entries
         self._ws: dict = {}
         self._w_host = None      # host copy of the weights last uploaded by weights()
         self._w_dev = None
-        self._graphs: dict = {}  # batch-1 CUDA graphs per configuration (infer_one)
+        # batch-1 CUDA graphs per configuration (infer_one), LRU of MAX_GRAPHS;
+        # each entry holds every device buffer its graph reads (table, image,
+        # counts, workspace), so a graph never outlives the memory it captured
+        self._graphs: OrderedDict = OrderedDict()
         self._pinned: dict = {}   # grow-only pinned host staging buffers
 
     # ------------------------------------------------------------ helpers
@@ -112,23 +120,25 @@ class Engine:
         torch = _torch()
         key = table_key(c)
         hit = self._tables.get(key)
-        if hit is None:
+        if hit is not None:
+            self._tables.move_to_end(key)
+        else:
             with torch.cuda.stream(self.stream):
                 ctab = torch.empty((c.n_steps, 256), dtype=torch.float64, device=self.device)
                 spk = torch.empty((c.n_steps, 256), dtype=torch.uint8, device=self.device)
             _native.check(self.lib.snn_input_table(ctypes.byref(c), ctab.data_ptr(), spk.data_ptr(), self.sptr))
             torch.cuda.current_stream(self.device).wait_stream(self.stream)
-            if len(self._tables) >= 8:
-                self._tables.pop(next(iter(self._tables)))
+            if len(self._tables) >= MAX_TABLES:
+                self._tables.popitem(last=False)   # graphs keep their own reference to it
             hit = self._tables[key] = (ctab, spk)
         return hit
 
     # ------------------------------------------------------------ inference
-    def infer(self, c, images, w, *, raster=False, trace=False, max_chunk=None):
+    def infer(self, c, images, w, *, raster=False, trace=False, ties=False, max_chunk=None):
         """Run n presentations.  images: uint8 [n,784] device tensor; w: f64
         [8112,10] device tensor.  Returns dict of device tensors (counts int32
         [n,10]; optionally raster/tile_pos/n_tiles/tile_base/out_raster,
-        ff/v_out/v_hid)."""
+        ff/v_out/v_hid, near_ties int32 [n] (snn_infer_out_t.near_ties))."""
         torch = _torch()
         n = int(images.shape[0])
         N = c.n_steps
@@ -143,6 +153,8 @@ class Engine:
                 out["n_tiles"] = torch.empty((n,), dtype=torch.int32, device=dev)
                 out["tile_base"] = torch.empty((n + 1,), dtype=torch.int32, device=dev)
                 out["out_raster"] = torch.empty((n, N), dtype=torch.int16, device=dev)
+            if ties:
+                out["near_ties"] = torch.empty((n,), dtype=torch.int32, device=dev)
             if trace:
                 out["ff"] = torch.empty((n, N, N_OUTPUTS), dtype=torch.float64, device=dev)
                 out["v_out"] = torch.empty((n, N, N_OUTPUTS), dtype=torch.float64, device=dev)
@@ -200,7 +212,11 @@ class Engine:
         d_w = self.weights(w, check) if w is not None else self._w_dev
         key = bytes(c)
         gr = self._graphs.get(key)
-        if gr is None:
+        if gr is not None:
+            self._graphs.move_to_end(key)
+        else:
+            if len(self._graphs) >= MAX_GRAPHS:
+                self._graphs.popitem(last=False)  # drops the graph with its buffers
             ctab, _ = self.table(c)
             with torch.cuda.stream(self.stream):
                 img_d = torch.zeros((1, N_INPUTS), dtype=torch.uint8, device=self.device)
@@ -221,7 +237,7 @@ class Engine:
                 img_d.copy_(img_h, non_blocking=True)
                 _native.check(self.lib.snn_infer(*args))
                 cnt_h.copy_(cnt_d, non_blocking=True)
-            gr = self._graphs[key] = {"g": g, "img": img_d, "cnt": cnt_d, "ws": ws, "c": c, "o": o,
+            gr = self._graphs[key] = {"g": g, "img": img_d, "cnt": cnt_d, "ws": ws, "c": c, "o": o, "ctab": ctab,
                                       "img_h": img_h, "cnt_h": cnt_h,
                                       "img_np": img_h.numpy()[0], "cnt_np": cnt_h.numpy()[0]}
         gr["img_np"][:] = image.reshape(-1)

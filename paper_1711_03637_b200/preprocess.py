@@ -7,8 +7,20 @@ crop to ink, longer side to 20 px with Pillow's BILINEAR resampling, place
 by centre of mass, 3x3 Gaussian blur) on the GPU (``k_preprocess`` through
 ``snn_preprocess``); ``preprocess_batch`` does many canvases in one launch.
 Outputs are bit-identical to the reference's; a canvas without ink raises
-``BlankDrawingError`` like the reference.  Canvases larger than 1024 px per
-side (the service's MAX_CANVAS_SIDE, service.py:31) are rejected.
+``BlankDrawingError`` like the reference.
+
+Host-side normalisation, exact by construction (everything after
+``binarize`` depends only on the ink mask, preprocess.py:110-115):
+* a uint8 canvas with a threshold t goes to the kernel as is with
+  ceil(t) (for integer pixels ``x >= t  <=>  x >= ceil(t)``);
+* any other dtype (float, int16, bool, ...) is binarized on the host with
+  the reference's own comparison ``canvas >= threshold`` and sent as a
+  0/255 mask with threshold 128;
+* a canvas wider or taller than the kernel's 1024 px is cropped on the host
+  to the ink's bounding box first (the reference crops to the same box,
+  preprocess.py:38-45, before anything else); only an INK extent beyond
+  1024 px per side is rejected (ValueError; the service itself caps canvases
+  at 1024 px, service.py:31).
 """
 from __future__ import annotations
 
@@ -43,25 +55,48 @@ def _as_canvas(canvas) -> np.ndarray:
     arr = np.asarray(canvas)
     if arr.ndim != 2 or arr.shape[0] < 1 or arr.shape[1] < 1:
         raise ValueError(f"canvas must be a 2-D grayscale array, got shape {arr.shape}")
-    if arr.shape[0] > MAX_SIDE or arr.shape[1] > MAX_SIDE:
-        raise ValueError(f"canvas {arr.shape} exceeds {MAX_SIDE} px per side")
-    return np.ascontiguousarray(arr, dtype=np.uint8) if arr.dtype != np.uint8 else np.ascontiguousarray(arr)
+    return arr
 
 
-def _thresholds(threshold, n: int) -> np.ndarray:
-    t = np.broadcast_to(np.asarray(threshold, dtype=np.int64), (n,))
-    if n and (t.min() < 0 or t.max() > 255):
+def _check_threshold(threshold):
+    """preprocess.py:31-35 (binarize): the same test, the same message."""
+    if not 0 <= threshold <= 255:
         raise ValueError("threshold must lie in 0..255")
-    return np.ascontiguousarray(t, dtype=np.int32)
+    return threshold
+
+
+def _prepare(canvas, threshold):
+    """(uint8 canvas <= 1024 px per side, int threshold) with the same ink
+    mask as ``canvas >= threshold`` (see the module docstring)."""
+    arr = _as_canvas(canvas)
+    thr = _check_threshold(threshold)
+    if arr.dtype == np.uint8:
+        t = int(np.ceil(thr))
+    else:  # the reference's own comparison, on the host
+        arr = np.where(arr >= thr, np.uint8(255), np.uint8(0))
+        t = 128
+    if arr.shape[0] > MAX_SIDE or arr.shape[1] > MAX_SIDE:
+        mask = arr >= t
+        rows, cols = np.flatnonzero(mask.any(axis=1)), np.flatnonzero(mask.any(axis=0))
+        if rows.size == 0:  # no ink (so t > 0): a 1x1 canvas without ink reports the blank drawing
+            arr = np.zeros((1, 1), dtype=np.uint8)
+        else:
+            arr = arr[rows[0]:rows[-1] + 1, cols[0]:cols[-1] + 1]
+        if arr.shape[0] > MAX_SIDE or arr.shape[1] > MAX_SIDE:
+            raise ValueError(f"ink extent {arr.shape} exceeds {MAX_SIDE} px per side")
+    return np.ascontiguousarray(arr), t
 
 
 def preprocess_batch(canvases, threshold=128):
     """Preprocess many canvases in one launch.  Returns (images uint8
     [n, 28, 28], blank bool [n]); blank canvases give an all-zero image."""
     from .engine import get_engine, _torch
-    cs = [_as_canvas(c) for c in canvases]
-    n = len(cs)
-    thr = _thresholds(threshold, n)
+    canvases = list(canvases)
+    n = len(canvases)
+    ts = list(np.broadcast_to(np.asarray(threshold, dtype=object), (n,))) if n else []
+    prep = [_prepare(c, t) for c, t in zip(canvases, ts)]
+    cs = [p[0] for p in prep]
+    thr = np.array([p[1] for p in prep], dtype=np.int32)
     if n == 0:
         return np.zeros((0, OUT_SIDE, OUT_SIDE), dtype=np.uint8), np.zeros(0, dtype=bool)
     shapes = np.array([c.shape for c in cs], dtype=np.int32)

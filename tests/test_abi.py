@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared_functions():
         assert hasattr(lib, name), name
     assert {s[0] for s in _native.SIGNATURES} == set(declared_functions())
-    assert lib.snn_abi_version() == 1
+    assert lib.snn_abi_version() == _native.ABI_VERSION == 2
 
 
 def test_workspace_queries_need_no_gpu():
@@ -67,9 +67,9 @@ def test_struct_layout_matches_c(tmp_path):
 #include <stddef.h>
 #include "snn_b200.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(snn_consts_t), offsetof(snn_consts_t, lif_hid),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(snn_consts_t), offsetof(snn_consts_t, lif_hid),
          offsetof(snn_consts_t, inhibition), offsetof(snn_consts_t, taps), sizeof(snn_lif_t),
-         sizeof(snn_infer_out_t), offsetof(snn_infer_out_t, v_hid));
+         sizeof(snn_infer_out_t), offsetof(snn_infer_out_t, v_hid), offsetof(snn_infer_out_t, near_ties));
   return 0;
 }
 ''')
@@ -78,7 +78,8 @@ int main(void) {
     got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()))
     C = _native.ConstsC
     want = [ctypes.sizeof(C), C.lif_hid.offset, C.inhibition.offset, C.taps.offset,
-            ctypes.sizeof(_native.LifC), ctypes.sizeof(_native.InferOutC), _native.InferOutC.v_hid.offset]
+            ctypes.sizeof(_native.LifC), ctypes.sizeof(_native.InferOutC), _native.InferOutC.v_hid.offset,
+            _native.InferOutC.near_ties.offset]
     assert got == want
 
 

@@ -64,3 +64,27 @@ def test_gpu_pipeline_single_and_errors(canvases):
     big[1023, 0] = 255
     from oracle import preprocess_oracle as P
     assert np.array_equal(sd.preprocess_pipeline(big), P.preprocess(big))
+
+
+def test_host_normalisation_keeps_the_reference_mask():
+    """preprocess._prepare (non-uint8 canvases, fractional thresholds, canvases
+    over 1024 px): the uint8 canvas and integer threshold it hands the kernel
+    give the reference's outputs (checked with the oracle's pipeline on CPU
+    against oracle/gen_canvases_extra.py's reference fixtures)."""
+    import os
+    from oracle import preprocess_oracle as P
+    from paper_1711_03637_b200.preprocess import MAX_SIDE, _prepare
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "canvases_extra.npz"))
+    for k in range(6):
+        cv, thr = z[f"canvas{k}"], float(z[f"threshold{k}"])
+        thr = int(thr) if thr.is_integer() else thr
+        arr, t = _prepare(cv, thr)
+        assert arr.dtype == np.uint8 and isinstance(t, int) and 0 <= t <= 255
+        assert max(arr.shape) <= MAX_SIDE
+        assert np.array_equal(P.preprocess(arr, t), z[f"out{k}"]), k
+    with pytest.raises(ValueError, match="threshold"):
+        _prepare(np.zeros((4, 4), np.uint8), 256)
+    with pytest.raises(ValueError, match="2-D"):
+        _prepare(np.zeros(4, np.uint8), 128)
+    blank, t = _prepare(np.zeros((1500, 20), np.uint8), 128)
+    assert blank.shape == (1, 1) and not (blank >= t).any()
