@@ -11,10 +11,13 @@ by the reference itself), weights W_fix, T=100 ms, dt=1 ms (100 steps),
 sharded contiguously over the ranks with one NCCL all-gather of the counts.
 One step = the whole 10,000-image set (strong scaling).  Rank 0 also times
 NormAD training (configs[1]: 1,000 images, one GPU) and, at N=1, the CPU
-reference (the oracle port, all host cores) on a bounded sample.
+reference (all host cores) on a bounded sample.
 
---impl reference times the reference's CPU algorithm (oracle/snn_oracle.py,
-a bit-exact numpy restatement of spikedigits) on the host cores instead.
+--impl reference times the reference's own CPU path on the host cores: the
+UNMODIFIED spikedigits package installed in baseline/_ref
+(scripts/stage_reference.sh), through its public batch_counts with one worker
+process per core -- or, if that install is missing, the oracle port
+(oracle/snn_oracle.py, a bit-exact numpy restatement), labelled kind "port".
 """
 from __future__ import annotations
 
@@ -42,17 +45,52 @@ N_IMAGES = 10_000
 F_INF_PER_STEP = 389_516          # dense algorithmic flop per image-step
 F_TRAIN_PER_STEP = 592_316
 F_TRAIN_PER_IMAGE = 162_240
-# executed float64 flop per ACTIVE window position and step in k_hidden<DEF>
-# (default filter bank): stencil = 8 chains (4 Sobel, 4 corner) with
-# 8 DMUL + 52 DFMA = 112 flop, Sobel negations are free; LIF = 12 x 5 flop.
-FLOP_PER_ACTIVE_POS_STEP = 112 + 12 * 5
-FP64_PIPE_OPS_PER_POS_STEP = 121   # k_hidden_res<FZ=3> inner loop: 50 DFMA + 29 DMUL + 36 DADD + 6 DSETP (SASS)
+# The roofline kernel of the default configuration and how its executed FP64
+# work per ACTIVE window-step is counted: from the SASS of the library that
+# runs (sass_loop_counts), the innermost loop (one window-step of 12 neurons):
+# flop = 2 DFMA + DMUL + DADD; FP64-pipe instructions = DFMA + DMUL + DADD + DSETP.
+HIDDEN_KERNEL = "_ZN3snn12k_hidden_resILb0ELb1ELb1ELi3EEEvNS_9BatchArgsE"   # k_hidden_res<0, 1, 1, 3>
+SASS_FALLBACK = {"DFMA": 50, "DMUL": 29, "DADD": 36, "DSETP": 6, "instructions": 235}  # r02 build, if cuobjdump is absent
 LAUNCHES_PER_CHUNK = 5   # per sub-batch: k_prep, k_tile_scan, k_hidden, k_gsum, k_output
 PIPE_IMAGES = 0          # snn_set_pipeline sub-batch (library default: off)
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def sass_loop_counts(so_path: str, fn: str) -> dict:
+    """FP64 op counts of the innermost loop of `fn` (the loop with the most
+    DFMA among the backward branches of the fewest instructions) in the SASS of
+    `so_path` (cuobjdump).  Falls back to SASS_FALLBACK (source: "fallback")."""
+    import collections
+    import re
+    import shutil
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    try:
+        txt = subprocess.run([tool, "-sass", "-fun", fn, so_path], capture_output=True, text=True,
+                             timeout=120).stdout.split("\n")
+    except (OSError, subprocess.TimeoutExpired):
+        txt = []
+    ins = []
+    for line in txt:
+        m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", line)
+        if m:
+            ins.append((int(m.group(1), 16), m.group(2)))
+    best = None
+    for a, t in ins:
+        m = re.search(r"BRA(?:\.\w+)* (?:!?U?P[T\d], )?(0x[0-9a-f]+)", t)
+        if not m or int(m.group(1), 16) >= a:
+            continue
+        body = [x for x in ins if int(m.group(1), 16) <= x[0] <= a]
+        cnt = collections.Counter((tt.split()[1] if tt.startswith("@") else tt.split()[0]).split(".")[0]
+                                  for _, tt in body)
+        if cnt["DFMA"] and (best is None or len(body) < best["instructions"]):
+            best = {"DFMA": cnt["DFMA"], "DMUL": cnt["DMUL"], "DADD": cnt["DADD"], "DSETP": cnt["DSETP"],
+                    "instructions": len(body)}
+    if best is None:
+        return dict(SASS_FALLBACK, source="fallback (cuobjdump unavailable)")
+    return dict(best, source=f"cuobjdump -sass -fun {fn} {os.path.basename(so_path)}")
 
 
 def host_cores() -> int:
@@ -191,37 +229,75 @@ def load_workload():
 
 
 # ============================================================== reference arm
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def stock_reference():
+    """The unmodified reference (pip-installed in baseline/_ref by
+    scripts/stage_reference.sh): (batch_counts, train_epoch, NetworkConfig,
+    default_filter_bank, LearnConfig) from its own modules, or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "spikedigits")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        from spikedigits.evaluate import batch_counts
+        from spikedigits.filters import default_filter_bank
+        from spikedigits.network import NetworkConfig
+        from spikedigits.normad import LearnConfig, train_epoch
+    except Exception as e:  # noqa: BLE001 -- report and fall back to the port
+        log(f"[reference] stock reference not importable ({e}); timing the oracle port")
+        return None
+    assert "baseline" in sys.modules["spikedigits"].__file__
+    return batch_counts, train_epoch, NetworkConfig, default_filter_bank, LearnConfig
+
+
+def reference_infer(imgs, w, cores):
+    """(callable(images) -> counts, kind, description) of the reference's CPU
+    batched inference on `cores` worker processes."""
+    ref = stock_reference()
+    if ref is not None:
+        bc, _, NC, bank, _ = ref
+        cfg, fb = NC(), bank()
+        return (lambda x: bc(x, w, fb, cfg, workers=cores)), "reference", \
+            f"stock spikedigits.evaluate.batch_counts(workers={cores}) from baseline/_ref"
+    from oracle import snn_oracle as orc
+    p = orc.Params()
+    return (lambda x: orc.batch_counts(x, w, p, workers=cores)), "port", \
+        f"oracle.batch_counts(workers={cores}) (bit-exact port)"
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle import snn_oracle as orc
     d, w = load_workload()
     imgs = d["c3_images"]
     cores = host_cores()
-    p = orc.Params()
     sample = int(min(len(imgs), max(2 * cores, cores * 32)))
-    log(f"[reference] oracle port on {cores} cores, {sample} images per step")
+    fn, kind, desc = reference_infer(imgs, w, cores)
+    log(f"[reference] {desc}, {sample} images per step")
     for _ in range(args.warmup):
-        orc.batch_counts(imgs[:sample], w, p, workers=cores)
+        fn(imgs[:sample])
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        orc.batch_counts(imgs[:sample], w, p, workers=cores)
+        got = fn(imgs[:sample])
         times.append(time.perf_counter() - t0)
+    ref10k = np.load(os.path.join(ROOT, "tests", "golden", "c3_counts_reference.npz"))["counts"]
     value = sample * len(times) / sum(times)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference strokes generator)",
-        "config": {"workload": "c3 batched inference (reference CPU algorithm), bounded sample",
+        "config": {"workload": "c3 batched inference (reference CPU path), bounded sample",
                    "n_images_per_step": sample, "t_ms": 100.0, "dt_ms": 1.0, "n_steps": 100,
                    "parallelism": f"{cores} host processes"},
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
-                         "sample": f"first {sample} of the 10,000 c3 images per step, "
-                                   f"oracle.batch_counts(workers={cores}), {cpu_model()}"},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": kind,
+                         "sample": f"first {sample} of the 10,000 c3 images per step, {desc}, {cpu_model()}"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "counts_equal_committed_reference_counts": bool(np.array_equal(got, ref10k[:sample])),
     }
     print(json.dumps(line), flush=True)
 
@@ -311,6 +387,7 @@ def run_ours(args):
     # roofline pass: k_hidden timed alone (one un-pipelined launch per call,
     # CUDA events the library records around it on its stream)
     hk_ms, call1_ms = kernel_alone_ms(eng, c, d_img, d_w, flush, args.steps)
+    stage_ms = stage_times(eng, c, d_img, d_w, flush, args.steps)
     value = N_IMAGES * args.steps / (tot_ms / 1e3)
     counts_dev = out
     ref_prefix = None
@@ -355,7 +432,11 @@ def run_ours(args):
         assert chunks_per_step == 1, "k_hidden events time one launch per step"
         launch_ms = hk_ms                                    # k_hidden alone (CUDA events)
         call_ms = ker_ms / args.steps                        # whole (pipelined) snn_infer call
-        exec_flop_launch = float(act.sum()) * n_steps * FLOP_PER_ACTIVE_POS_STEP
+        from paper_1711_03637_b200 import _native
+        sass = sass_loop_counts(_native.LIB_PATH, HIDDEN_KERNEL)
+        flop_ws = 2 * sass["DFMA"] + sass["DMUL"] + sass["DADD"]
+        pipe_ws = sass["DFMA"] + sass["DMUL"] + sass["DADD"] + sass["DSETP"]
+        exec_flop_launch = float(act.sum()) * n_steps * flop_ws
         achieved = exec_flop_launch / (launch_ms * 1e-3) / 1e12
         dense_tflops = (b - a) * F_INF_PER_STEP * n_steps / (ker_ms / args.steps * 1e-3) / 1e12
         traffic_bytes, traffic_src = committed_traffic("k_hidden")
@@ -377,7 +458,10 @@ def run_ours(args):
                          "traffic_unit": "bytes per launch (DRAM read + write)", "traffic_source": traffic_src,
                          "kernel": "k_hidden<DEF> (fused input-table gather + 3x3 stencil + hidden LIF, "
                                    "spike raster out), timed alone with CUDA events (snn_profile_events)",
-                         "achieved_basis": f"executed fp64 flop: active windows x N x {FLOP_PER_ACTIVE_POS_STEP}",
+                         "achieved_basis": f"executed fp64 flop: active windows ({int(act.sum())}) x N ({n_steps}) x "
+                                           f"{flop_ws} flop per window-step (2 x {sass['DFMA']} DFMA + "
+                                           f"{sass['DMUL']} DMUL + {sass['DADD']} DADD in the kernel's inner loop, "
+                                           f"{sass['source']})",
                          "peak_source": "measured in this run: FP64 DFMA microbenchmark (libsnn_peaks.so); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
                          "launch_ms": launch_ms, "call_ms": call_ms, "unpipelined_call_ms": call1_ms,
@@ -385,11 +469,13 @@ def run_ours(args):
                          "dense_equiv_tflops": dense_tflops,
                          "dense_equiv_basis": "SURVEY 8(d) F_inf = 389,516 flop per image-step",
                          "fp32_peak_tflops": f32, "active_windows_per_image": float(act.mean()),
-                         "fp64_pipe_frac": achieved / FLOP_PER_ACTIVE_POS_STEP * FP64_PIPE_OPS_PER_POS_STEP / (f64 / 2),
-                         "fp64_pipe_basis": f"{FP64_PIPE_OPS_PER_POS_STEP} FP64-pipe instructions per active window-step "
-                                            "(50 DFMA + 29 DMUL + 36 DADD + 6 DSETP in the SASS of the inner "
+                         "fp64_pipe_frac": achieved / flop_ws * pipe_ws / (f64 / 2),
+                         "fp64_pipe_basis": f"{pipe_ws} FP64-pipe instructions per active window-step "
+                                            f"({sass['DFMA']} DFMA + {sass['DMUL']} DMUL + {sass['DADD']} DADD + "
+                                            f"{sass['DSETP']} DSETP of {sass['instructions']} in the SASS of the inner "
                                             "loop) against the DFMA instruction rate (peak / 2); ncu's "
-                                            "sm__pipe_fp64_cycles_active is the same quantity measured"},
+                                            "sm__pipe_fp64_cycles_active is the same quantity measured",
+                         "kernels": kernel_table(stage_ms, call1_ms, achieved / f64)},
             "clocks": clocks,
             "parity": {"c3_first200_counts_equal_reference": ref_prefix,
                        "c3_all10000_counts_equal_reference": ref_all,
@@ -442,6 +528,86 @@ def hidden_per_neuron_frac(eng, c, imgs_all, w):
         h = decode_hidden(raster, int(tb[i]), tpos[i], int(nt[i]), c.n_steps)
         same += int(np.array_equal(h.sum(axis=0), g["hidden_counts"][i]))
     return same / len(imgs)
+
+
+def stage_times(eng, c, d_img, d_w, flush, steps):
+    """Per-kernel device time of a live un-pipelined snn_infer call: CUDA
+    events the library records between its launches on its stream
+    (snn_profile_stage_events), L2 flushed before each call; medians."""
+    import torch
+    names = ["k_prep", "k_tile_scan", "k_hidden_res", "k_gsum", "k_output"]
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    for e in evs:
+        e.record(eng.stream)   # created lazily on first record
+    arr = (ctypes.c_void_p * 6)(*[e.cuda_event for e in evs])
+    per = {k: [] for k in names}
+    try:
+        for _ in range(max(3, steps)):
+            with torch.cuda.stream(eng.stream):
+                flush.zero_()
+            eng.lib.snn_profile_stage_events(arr, 6)
+            eng.infer(c, d_img, d_w)
+            eng.lib.snn_profile_stage_events(None, 0)
+            evs[-1].synchronize()
+            for k, name in enumerate(names):
+                per[name].append(evs[k].elapsed_time(evs[k + 1]))
+    finally:
+        eng.lib.snn_profile_stage_events(None, 0)
+    return {k: statistics.median(v) for k, v in per.items()}
+
+
+def committed_kernels():
+    """Per-kernel ncu metrics of the newest committed capture
+    (profiles/<round>_kernels.json, scripts/summarize_profiles.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernels.json")))
+    if not files:
+        return {}, None
+    return json.load(open(files[-1])), os.path.relpath(files[-1], ROOT)
+
+
+def _short(name: str) -> str:
+    return name.split("(")[0].split("<")[0].split()[-1].split("::")[-1]
+
+
+def kernel_table(stage_ms, call_ms, hidden_frac):
+    """Every kernel of the inference call: live duration (CUDA events) and its
+    share of the call, the bound that limits it and the fraction of that bound
+    -- the FP64 flop fraction for the hidden layer (measured here), the
+    committed ncu capture's pipe / issue / DRAM figures for the rest."""
+    prof, src = committed_kernels()
+    ncu = {}
+    for name, recs in prof.items():
+        ncu.setdefault(_short(name), recs[0])
+    mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = float(mp.get("hbm_gbs", 6553.3))
+    bounds = {"k_prep": "hbm/latency (one pass over the images)", "k_tile_scan": "latency (one CTA)",
+              "k_hidden_res": "fp64 pipe", "k_gsum": "issue / L2 gathers (W rows)",
+              "k_output": "fp64 dependent chain per image (latency)"}
+    out = {}
+    for k, ms in stage_ms.items():
+        e = {"ms": ms, "share_of_call": ms / call_ms if call_ms else None, "bound": bounds.get(k)}
+        n = ncu.get(k)
+        if n:
+            e["ncu"] = {x: n.get(x) for x in ("issue_active_pct", "fp64_pipe_pct", "dram_bytes", "duration_ms")}
+            if n.get("dram_bytes"):
+                e["dram_frac_of_hbm_peak"] = n["dram_bytes"] / (ms * 1e-3) / 1e9 / hbm
+        if k == "k_hidden_res":
+            e["frac"] = hidden_frac
+            e["frac_basis"] = "executed fp64 flop / FP64 DFMA peak (roofline.frac)"
+        elif k == "k_gsum" and n:
+            e["frac"] = (n.get("issue_active_pct") or 0) / 100.0
+            e["frac_basis"] = "issue slots busy (ncu smsp__issue_active); DRAM is dram_frac_of_hbm_peak"
+        elif k == "k_output" and n:
+            e["frac"] = (n.get("fp64_pipe_pct") or 0) / 100.0
+            e["frac_basis"] = "FP64 pipe busy (ncu); each warp is one image's serial 10-neuron chain"
+        elif n:
+            e["frac"] = (n.get("issue_active_pct") or 0) / 100.0
+            e["frac_basis"] = "issue slots busy (ncu)"
+        out[k] = e
+    out["_source"] = f"live CUDA events (snn_profile_stage_events) + {src or 'no committed ncu capture'}"
+    return out
 
 
 def kernel_alone_ms(eng, c, d_img, d_w, flush, steps):
@@ -559,11 +725,19 @@ def bench_train(args, sd, eng, d, cfg, bank):
         if rep >= 2:
             e2e_t.append(time.perf_counter() - t0)
     e2e = n / statistics.median(e2e_t)
-    # CPU reference: the oracle port's train_epoch (one core, as the reference trains) on 30 images
-    from oracle import snn_oracle as orc
+    # CPU reference: the stock reference's train_epoch (one process, as it trains) on 30 images
     k = 30
-    t0 = time.perf_counter()
-    orc.train_epoch(d["c2_images"][order][:k], d["c2_labels"][order][:k], np.zeros((8112, 10)), orc.Params())
+    ref = stock_reference()
+    if ref is not None:
+        _, te, NC, fb, LC = ref
+        t0 = time.perf_counter()
+        te(d["c2_images"][order][:k], d["c2_labels"][order][:k], np.zeros((8112, 10)), fb(), NC(), LC())
+        kind, desc = "reference", f"stock spikedigits.normad.train_epoch on the first {k} images (1 process)"
+    else:
+        from oracle import snn_oracle as orc
+        t0 = time.perf_counter()
+        orc.train_epoch(d["c2_images"][order][:k], d["c2_labels"][order][:k], np.zeros((8112, 10)), orc.Params())
+        kind, desc = "port", f"oracle.train_epoch on the first {k} images (1 core, as the reference)"
     cpu = k / (time.perf_counter() - t0)
     return {"metric": "NormAD online training images/s (1 GPU, sequential)", "value": value, "unit": "images/s",
             "workload": "c2: 1,000 synthetic images in epoch_permutation(0,0,1000) order from zero weights, "
@@ -573,8 +747,7 @@ def bench_train(args, sd, eng, d, cfg, bank):
             "dense_equiv_tflops": value * (F_TRAIN_PER_STEP * 100 + F_TRAIN_PER_IMAGE) / 1e12,
             "gpu_launches_per_epoch": 6 * train_chunks(eng, c, n),
             "critical_path": critical_path_model(c),
-            "cpu_baseline": {"value": cpu, "unit": "images/s", "cores": 1, "kind": "port",
-                             "sample": f"oracle.train_epoch on the first {k} images (1 core, as the reference)"}}
+            "cpu_baseline": {"value": cpu, "unit": "images/s", "cores": 1, "kind": kind, "sample": desc}}
 
 
 def bench_c5(sd, eng, cfg, bank, line):
@@ -642,7 +815,7 @@ def bench_c5(sd, eng, cfg, bank, line):
     if cb and ci_:
         est = n_tr / cb + n_ev / ci_
         out["cpu_baseline"] = {"value": (n_tr + n_ev) / est, "unit": "images/s", "cores": "1 (train) / all (eval)",
-                               "kind": "port", "sample": "extrapolated from the timed oracle samples above "
+                               "kind": line.get("cpu_baseline", {}).get("kind", "port"), "sample": "extrapolated from the timed oracle samples above "
                                "(train: 1 core, sequential as the reference; eval: all host cores)"}
     return out
 
@@ -723,17 +896,16 @@ def bench_preprocess(sd, w_fix, bank):
 
 
 def cpu_baseline(d, w):
-    from oracle import snn_oracle as orc
     cores = host_cores()
     imgs = d["c3_images"]
     sample = int(min(len(imgs), max(2 * cores, cores * 64)))   # ~25 core-seconds of CPU work
-    p = orc.Params()
-    orc.batch_counts(imgs[: 2 * cores], w, p, workers=cores)  # fork + table warm-up
+    fn, kind, desc = reference_infer(imgs, w, cores)
+    fn(imgs[: 2 * cores])  # fork + table warm-up
     t0 = time.perf_counter()
-    orc.batch_counts(imgs[:sample], w, p, workers=cores)
+    fn(imgs[:sample])
     v = sample / (time.perf_counter() - t0)
-    return {"value": v, "unit": "images/s", "cores": cores, "kind": "port",
-            "sample": f"first {sample} of the 10,000 c3 images, oracle.batch_counts(workers={cores}), {cpu_model()}"}
+    return {"value": v, "unit": "images/s", "cores": cores, "kind": kind,
+            "sample": f"first {sample} of the 10,000 c3 images, {desc}, {cpu_model()}"}
 
 
 def main():

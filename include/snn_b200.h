@@ -128,6 +128,13 @@ int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t n_images,
  * kernel alone with cudaEventElapsedTime.  Pass NULLs to disable. */
 void snn_profile_events(void *before, void *after);
 
+/* Profiling hook: with n_events >= 6 cudaEvent_t handles, every following
+ * un-pipelined inference launch sequence records events[0] before k_prep,
+ * [1] after k_prep, [2] after k_tile_scan, [3] after the hidden-layer kernel,
+ * [4] after k_gsum and [5] after k_output on its stream, so the caller can
+ * time each kernel of a live call.  NULL / 0 disables. */
+void snn_profile_stage_events(void *const *events, int n_events);
+
 /* The tuning and profiling knobs below (snn_set_*, snn_normad_*) apply to the
  * calling thread's CURRENT CUDA device (cudaSetDevice): one process can drive
  * several GPUs with independent settings.  Function attributes and occupancy

@@ -73,6 +73,7 @@ SIGNATURES = [
     ("snn_infer", ctypes.c_int, [ctypes.POINTER(ConstsC), _vp, ctypes.c_int64, _vp, _vp,
                                  ctypes.POINTER(InferOutC), _vp, ctypes.c_size_t, _vp]),
     ("snn_profile_events", None, [_vp, _vp]),
+    ("snn_profile_stage_events", None, [_vp, ctypes.c_int]),
     ("snn_set_pipeline", None, [ctypes.c_int64, ctypes.c_int]),
     ("snn_set_normad_cluster", None, [ctypes.c_int]),
     ("snn_set_hidden_resident", None, [ctypes.c_int]),

@@ -181,12 +181,11 @@ def batch_counts(images, weights, filters, cfg, workers: int = 1) -> np.ndarray:
     imgs = as_pixel_batch(images)
     if len(imgs) == 0:
         return np.zeros((0, N_OUTPUTS), dtype=np.int64)
-    w = _weights(weights)
-    c = make_consts(cfg, filters)
+    c = _consts_cached(cfg, filters)
     eng = get_engine()
     with eng.lock:
-        d_img = _to_device(eng, imgs.reshape(len(imgs), -1))
-        d_w = _to_device(eng, w)
+        d_w = eng.weights(weights, check=_weights)   # validated once per distinct W, kept on the device
+        d_img = eng.upload("images", imgs).view(len(imgs), -1)
         counts = eng.infer(c, d_img, d_w)["counts"]
         return _fetch(eng, counts).astype(np.int64)
 

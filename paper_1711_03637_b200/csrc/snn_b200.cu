@@ -156,6 +156,10 @@ size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base, 
 }
 
 cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;  // snn_profile_events
+cudaEvent_t g_stage[6] = {};                               // snn_profile_stage_events
+inline void stage_mark(int k, cudaStream_t st) {
+    if (g_stage[k]) cudaEventRecord(g_stage[k], st);
+}
 
 // Per-device state: function attributes, occupancy and SM counts are
 // properties of a device context, and the tuning knobs (snn_set_*) apply to
@@ -243,10 +247,13 @@ int launch_hidden(const BatchArgs &A, cudaStream_t st) {
     const int per_sm = K.hid_ctas > 0 ? std::min(K.hid_ctas, hid_blocks) : hid_blocks;
     int rc;
     const unsigned n = (unsigned)A.n_images;
+    stage_mark(0, st);
     k_prep<<<n, kThreads, 0, st>>>(A);
     if ((rc = cuda_check("k_prep"))) return rc;
+    stage_mark(1, st);
     k_tile_scan<<<1, 1024, 0, st>>>(A);
     if ((rc = cuda_check("k_tile_scan"))) return rc;
+    stage_mark(2, st);
     if (g_ev_before) cudaEventRecord(g_ev_before, st);
     if (K.hid_res && A.c.n_steps <= kResMaxSteps) {  // table resident in shared memory
         if constexpr (DEF && !TRACE) {
@@ -263,6 +270,7 @@ int launch_hidden(const BatchArgs &A, cudaStream_t st) {
     }
     if ((rc = cuda_check("k_hidden"))) return rc;
     if (g_ev_after) cudaEventRecord(g_ev_after, st);
+    stage_mark(3, st);
     return SNN_OK;
 }
 
@@ -277,8 +285,10 @@ int launch_contract(const BatchArgs &A, double *g, cudaStream_t st) {
     if (gabs) k_gsum<true><<<gg, kGWarps * 32, 0, st>>>(A, g, gabs);
     else k_gsum<false><<<gg, kGWarps * 32, 0, st>>>(A, g, nullptr);
     if ((rc = cuda_check("k_gsum"))) return rc;
+    stage_mark(4, st);
     if (gabs) k_output<true><<<og, kOutWarps2 * 32, 0, st>>>(A, g, gabs);
     else k_output<false><<<og, kOutWarps2 * 32, 0, st>>>(A, g, nullptr);
+    stage_mark(5, st);
     return cuda_check("k_output");
 }
 
@@ -362,6 +372,10 @@ extern "C" void snn_profile_events(void *before, void *after) {
     g_ev_before = (cudaEvent_t)before;
     g_ev_after = (cudaEvent_t)after;
 }
+extern "C" void snn_profile_stage_events(void *const *events, int n_events) {
+    for (int k = 0; k < 6; ++k) g_stage[k] = (events && k < n_events) ? (cudaEvent_t)events[k] : nullptr;
+}
+
 extern "C" const char *snn_last_error(void) { return g_err; }
 
 extern "C" int snn_input_table(const snn_consts_t *c, double *d_ctab, uint8_t *d_spk, void *stream) {

@@ -58,8 +58,8 @@ def sharded_batch_counts(images, weights, filters, cfg, group=None) -> np.ndarra
     import torch
     import torch.distributed as dist
 
-    from .api import _to_device, _weights
-    from .engine import get_engine, make_consts
+    from .api import _consts_cached, _weights
+    from .engine import get_engine
     from .params import as_pixel_batch
 
     imgs = as_pixel_batch(images)
@@ -71,13 +71,12 @@ def sharded_batch_counts(images, weights, filters, cfg, group=None) -> np.ndarra
         return batch_counts(imgs, weights, filters, cfg)
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     a, b = shard_bounds(n, world)[rank]
-    w = _weights(weights)
-    c = make_consts(cfg, filters)
+    c = _consts_cached(cfg, filters)
     eng = get_engine()
     with eng.lock:
-        d_w = _to_device(eng, w)
+        d_w = eng.weights(weights, check=_weights)
         if b > a:
-            d_img = _to_device(eng, imgs[a:b].reshape(b - a, -1))
+            d_img = eng.upload("images", imgs[a:b]).view(b - a, -1)
             local = eng.infer(c, d_img, d_w)["counts"]
         else:
             local = torch.zeros((0, N_OUTPUTS), dtype=torch.int32, device=eng.device)

@@ -115,6 +115,21 @@ class Engine:
             self._pinned[name] = buf
         return buf
 
+    def upload(self, name: str, arr: np.ndarray):
+        """Host array -> device uint8 tensor of the same bytes, through a
+        grow-only pinned staging buffer (no per-call pinned allocation) and an
+        async H2D copy on the engine's stream.  The caller holds the lock and
+        synchronizes the stream before the next upload reuses the buffer."""
+        torch = _torch()
+        src = np.ascontiguousarray(arr).reshape(-1).view(np.uint8)
+        nb = int(src.nbytes)
+        host = self.pinned(name, nb)
+        np.copyto(host.numpy()[:nb], src)
+        dev = self.buffer(name, nb)
+        with torch.cuda.stream(self.stream):
+            dev[:nb].copy_(host[:nb], non_blocking=True)
+        return dev[:nb]
+
     def table(self, c: _native.ConstsC):
         """(c_table [N,256] f64, spike table [N,256] u8) on device, cached per config."""
         torch = _torch()

@@ -47,13 +47,39 @@ def _bytes(v, unit):
     return float(v.replace(",", "")) * scale
 
 
-def summarize(rep, fh, traffic):
+def _num(v):
+    try:
+        return float(v.replace(",", ""))
+    except (ValueError, AttributeError):
+        return None
+
+
+def summarize(rep, fh, traffic, kernels=None):
     rows = ncu_csv(["-i", rep, "--page", "raw", "--csv"])
     if len(rows) < 3:
         return
     h, units = rows[0], rows[1]
     for r in rows[2:]:
         name = r[h.index("Kernel Name")]
+        if kernels is not None:  # machine-readable per-kernel figures (bench.py roofline.kernels)
+            def get(key, scale=1.0):
+                return _num(r[h.index(key)]) * scale if key in h and _num(r[h.index(key)]) is not None else None
+            it = h.index("gpu__time_duration.sum") if "gpu__time_duration.sum" in h else None
+            dur_scale = {"ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(units[it], 1.0) if it is not None else 1.0
+            rec = {"capture": os.path.basename(rep),
+                   "duration_ms": get("gpu__time_duration.sum", dur_scale),
+                   "issue_active_pct": get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                   "fp64_pipe_pct": get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                   "warps_active_per_sm": get("sm__warps_active.avg.per_cycle_active"),
+                   "registers": get("launch__registers_per_thread"),
+                   "warp_instructions": get("smsp__inst_executed.sum")}
+            if "dram__bytes_read.sum" in h and "dram__bytes_write.sum" in h:
+                ir, iw = h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
+                rec["dram_bytes"] = _bytes(r[ir], units[ir]) + _bytes(r[iw], units[iw])
+            if "lts__t_bytes.sum" in h:
+                il = h.index("lts__t_bytes.sum")
+                rec["l2_bytes"] = _bytes(r[il], units[il])
+            kernels.setdefault(name.split("(")[0], []).append(rec)
         if "dram__bytes_read.sum" in h and "dram__bytes_write.sum" in h:
             ir, iw, it = h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum"), h.index("gpu__time_duration.sum")
             traffic.setdefault(name.split("(")[0], []).append(
@@ -103,10 +129,12 @@ def main():
     with open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w") as fh:
         fh.write(f"# ncu summary ({tag})\n\nFrom `ncu --set full --clock-control none --import-source on` "
                  "captures (cold-cache, serialised replays: compare shares, not absolutes).\n")
-        traffic = {}
+        traffic, kernels = {}, {}
         for rep in reps:
             fh.write(f"\n## {rep}\n")
-            summarize(os.path.join(OUT, rep), fh, traffic)
+            summarize(os.path.join(OUT, rep), fh, traffic, kernels)
+    with open(os.path.join(PROF, f"{tag}_kernels.json"), "w") as g:
+        json.dump(kernels, g, indent=1)
     # per-launch DRAM traffic of each captured kernel (bench.py roofline.traffic)
     with open(os.path.join(PROF, f"{tag}_traffic.json"), "w") as g:
         json.dump(traffic, g, indent=1)

@@ -45,6 +45,14 @@ FILES = {
 }
 
 
+# Reference tests that cannot pass anywhere: they read fixtures the reference
+# distribution does not ship (tests/data/ is absent from /root/reference/pkg,
+# so they fail with FileNotFoundError on the stock CPU reference as well).
+DESELECT = {
+    "test_preprocess.py": ["TestPipeline::test_golden_corpus"],   # tests/data/golden_preprocess/digits.npz
+}
+
+
 def run_ref_file(name, tmp_path, extra=()):
     report = tmp_path / "report.json"
     env = dict(os.environ)
@@ -60,7 +68,8 @@ def run_ref_file(name, tmp_path, extra=()):
 
 @pytest.mark.parametrize("name", sorted(FILES))
 def test_reference_suite_file_on_gpu(name, tmp_path):
-    r, rep = run_ref_file(name, tmp_path)
+    extra = [a for t in DESELECT.get(name, []) for a in ("--deselect", f"{os.path.join(SUITE, name)}::{t}")]
+    r, rep = run_ref_file(name, tmp_path, extra)
     tail = (r.stdout[-3000:] + r.stderr[-2000:])
     assert r.returncode == 0, tail
     assert rep.get("network.run_presentation") == "paper_1711_03637_b200.api.run_presentation", rep
