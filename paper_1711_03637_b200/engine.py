@@ -116,18 +116,18 @@ class Engine:
         return buf
 
     def upload(self, name: str, arr: np.ndarray):
-        """Host array -> device uint8 tensor of the same bytes, through a
-        grow-only pinned staging buffer (no per-call pinned allocation) and an
-        async H2D copy on the engine's stream.  The caller holds the lock and
-        synchronizes the stream before the next upload reuses the buffer."""
+        """Host array -> device uint8 tensor of the same bytes (grow-only
+        device buffer `name`), copied straight from the caller's pageable
+        memory on the engine's stream: the driver stages and DMAs it in
+        pipelined chunks, measured faster on B200 hosts than a host copy into
+        pinned memory followed by a pinned H2D (0.39 vs 0.39 + 0.34 ms for
+        7.8 MB, scripts/e2e_breakdown.py).  The caller holds the lock."""
         torch = _torch()
         src = np.ascontiguousarray(arr).reshape(-1).view(np.uint8)
         nb = int(src.nbytes)
-        host = self.pinned(name, nb)
-        np.copyto(host.numpy()[:nb], src)
         dev = self.buffer(name, nb)
         with torch.cuda.stream(self.stream):
-            dev[:nb].copy_(host[:nb], non_blocking=True)
+            dev[:nb].copy_(torch.from_numpy(src), non_blocking=True)
         return dev[:nb]
 
     def table(self, c: _native.ConstsC):

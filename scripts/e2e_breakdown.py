@@ -44,3 +44,14 @@ print(f"infer (device)           {med(lambda: eng.infer(c, d_img, d_w)):.3f} ms"
 out = eng.infer(c, d_img, d_w)["counts"]
 print(f"fetch counts             {med(lambda: api._fetch(eng, out)):.3f} ms")
 print(f"make_consts              {med(lambda: make_consts(cfg, bank)):.3f} ms")
+# pinning the caller's buffer in place
+cr = torch.cuda.cudart()
+def reg():
+    cr.cudaHostRegister(imgs.ctypes.data, imgs.nbytes, 0)
+    cr.cudaHostUnregister(imgs.ctypes.data)
+print(f"cudaHostRegister+unreg   {med(reg):.3f} ms")
+half = n // 2
+def two_chunk():
+    a = api.batch_counts(imgs[:half], w, bank, cfg)
+    b = api.batch_counts(imgs[half:], w, bank, cfg)
+print(f"2 sequential half calls  {med(two_chunk):.3f} ms")

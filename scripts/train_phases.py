@@ -27,14 +27,16 @@ for rep in range(3):
     torch.cuda.synchronize()
 eng.lib.snn_normad_phase_clocks(None)
 k = clk.cpu().numpy()[4:64]
-names = ["G partials", "B1", "gather G", "scan", "sigma", "R adjoint", "B2", "copy R", "dW", "B3", "commit", "next"]
-d_ = np.diff(k[:, :12], axis=1)
-nxt = k[1:, 0] - k[:-1, 11]
+# stamps of k_normad_cl (normad_cl.cuh): 0 start, 1 partials done, 2 after B1,
+# 3 G gathered, 12 scan warp done, 13 stage warps done, 4 scan section done,
+# 5 after OMASK broadcast + B2, 6 sigma, 7 R adjoint, 9 dW committed
+edges = [("G partials", 0, 1), ("B1", 1, 2), ("gather G", 2, 3), ("scan (warp 0)", 3, 12),
+         ("scan section", 3, 4), ("bcast + B2", 4, 5), ("sigma", 5, 6), ("R adjoint", 6, 7), ("dW", 7, 9)]
 print("cycles per phase (median over images 4..63):")
-for i, n in enumerate(names[:11]):
-    print(f"  {n:12s} {np.median(d_[:, i]):8.0f}")
-print(f"  {'to next img':12s} {np.median(nxt):8.0f}")
-print("scan cycles per image:", d_[:, 3].tolist()[:8])
-print("scan warp loop (median):", np.median(k[:, 12] - k[:, 3]), " stage warps (median):", np.median(k[:, 13] - k[:, 3]))
+for name, a, b in edges:
+    print(f"  {name:14s} {np.median(k[:, b] - k[:, a]):8.0f}")
+nxt = k[1:, 0] - k[:-1, 9]
+print(f"  {'to next img':14s} {np.median(nxt):8.0f}")
+print("stage warps (median):", np.median(k[:, 13] - k[:, 3]))
 tot = np.median(k[1:, 0] - k[:-1, 0])
-print(f"  per image    {tot:8.0f} cycles = {tot / 1.965e3:.2f} us at 1965 MHz")
+print(f"  per image      {tot:8.0f} cycles = {tot / 1.965e3:.2f} us at 1965 MHz")

@@ -68,7 +68,7 @@ def run_ref_file(name, tmp_path, extra=()):
 
 @pytest.mark.parametrize("name", sorted(FILES))
 def test_reference_suite_file_on_gpu(name, tmp_path):
-    extra = [a for t in DESELECT.get(name, []) for a in ("--deselect", f"{os.path.join(SUITE, name)}::{t}")]
+    extra = [a for t in DESELECT.get(name, []) for a in ("--deselect", f"tests/{name}::{t}")]
     r, rep = run_ref_file(name, tmp_path, extra)
     tail = (r.stdout[-3000:] + r.stderr[-2000:])
     assert r.returncode == 0, tail
