@@ -103,6 +103,9 @@ typedef struct snn_infer_out {
                             event-driven sum, propagated through the LIF update
                             (DESIGN.md section 6.1).  0 on an image means its
                             output spikes are provably the reference's. */
+    int32_t *hidden_redo;/* [1] windows the guard-band hidden kernel re-simulated
+                            in float64; written by the last
+                            hidden-layer launch of the call */
 } snn_infer_out_t;
 
 int snn_abi_version(void);
@@ -148,13 +151,16 @@ void snn_profile_stage_events(void *const *events, int n_events);
  * no gain on one B200 -- the persistent k_hidden leaves no room to overlap). */
 void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_per_sm);
 
-/* The hidden-layer kernel keeps the whole input table in shared memory (one
- * CTA of 20 warps per SM, no per-chunk barriers) when N <= 108 (enable = 1,
- * default), else it streams the table through a ring; enable = 0 forces the
- * ring kernel (same results).  With the default bank and a refractory span of
- * 3 steps at every step (t_ref/dt = 3) the resident kernel tracks refractory
- * neurons by the window's last three spike masks; enable = 2 keeps the
- * per-neuron refractory horizons instead (same results; for A/B). */
+/* Hidden-layer kernel selection (all give the same raster bits).  Default
+ * (enable = 1): with the default bank, a refractory span of 3 steps at every
+ * step (t_ref/dt = 3) and N <= 200, the guard-band kernel -- float32 packed
+ * pairs with a per-window float64 error bound, windows near a threshold
+ * decision re-simulated in float64; otherwise the float64
+ * kernel that keeps the whole input table in shared memory (one CTA of 20
+ * warps per SM) when N <= 108, else the one that streams the table through a
+ * ring.  enable = 3: the float64 table-resident kernel (frozen spike masks)
+ * instead of the guard-band kernel; enable = 2: float64 with per-neuron
+ * refractory horizons; enable = 0: the float64 ring kernel. */
 void snn_set_hidden_resident(int enable);
 
 /* snn_train runs its sequential NormAD chain on a cluster of 8 CTAs that

@@ -61,7 +61,7 @@ class ConstsC(ctypes.Structure):
 class InferOutC(ctypes.Structure):
     _fields_ = [(name, _vp) for name in
                 ("counts", "raster", "tile_pos", "n_tiles", "tile_base", "out_raster", "ff", "v_out", "v_hid",
-                 "near_ties")]
+                 "near_ties", "hidden_redo")]
 
 
 # (name, restype, argtypes) -- one row per declaration in include/snn_b200.h

@@ -72,6 +72,8 @@ struct BatchArgs {
     int32_t items_per_tile;  // 1 (default bank) or 2 (generic bank)
     snn_infer_out_t out;     // counts / out_raster / ff / v_out / v_hid / near_ties
     double *gabs;            // [n][N][10] |W| sums (near_ties only)
+    int32_t *fix_count;      // guard-band hidden layer (hidden_gb.cuh): flagged windows
+    int32_t *fix_list;       // [n * 676] their indices in the compacted window list
 };
 
 __device__ __forceinline__ uint64_t warp_excl_scan_u64(uint64_t x, uint64_t *total) {
@@ -172,6 +174,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const BatchArgs A) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n = A.n_images;
     if (tid < 2) s_carry[tid] = 0;
+    if (tid == 0 && A.fix_count) *A.fix_count = 0;  // the guard-band kernel's work list (hidden_gb.cuh)
     __syncthreads();
     for (int64_t base = 0; base < n; base += 1024 * kPer) {
         const int64_t i0 = base + (int64_t)tid * kPer;
@@ -470,14 +473,15 @@ __device__ __forceinline__ int hidden_items(const BatchArgs &A, int ipt) {
     return ipt * ((A.win_base[A.n_images] + kTile - 1) / kTile);
 }
 
-template <bool DEF>
-__device__ __forceinline__ void item_setup(const BatchArgs &A, int item, int total, int nchunks, ItemState &it) {
-    const int lane = threadIdx.x & 31;
+// One window of the batch (gw: index in the batch's compacted window list,
+// image after image): its image, position, pixel levels and raster slot.
+// `live` is warp-uniform (the work item exists); lanes past the batch's last
+// window get pos = 0xFFFF (on = false).
+__device__ __forceinline__ void window_setup(const BatchArgs &A, bool live, int gw, int half, int nchunks,
+                                             ItemState &it) {
     const int64_t n = A.n_images;
-    it.live = item < total;  // warp-uniform
-    const int grp = DEF ? item : item >> 1;
-    it.half = DEF ? 0 : item & 1;
-    const int gw = grp * kTile + lane;  // this lane's window in the batch
+    it.live = live;
+    it.half = half;
     it.img = 0;
     it.pos = 0xFFFF;
     it.rout = nullptr;
@@ -510,6 +514,13 @@ __device__ __forceinline__ void item_setup(const BatchArgs &A, int item, int tot
             const uint32_t lev = it.on ? __ldg(im + (r + a) * kSide + col + b) : 0u;
             it.lvp[k >> 2] |= lev << (8 * (k & 3));
         }
+}
+
+template <bool DEF>
+__device__ __forceinline__ void item_setup(const BatchArgs &A, int item, int total, int nchunks, ItemState &it) {
+    const int lane = threadIdx.x & 31;
+    const int grp = DEF ? item : item >> 1;
+    window_setup(A, item < total, grp * kTile + lane, DEF ? 0 : item & 1, nchunks, it);
 }
 
 // The steps of one chunk for one live item (tab = the chunk's [8][256] table

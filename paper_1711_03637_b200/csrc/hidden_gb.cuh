@@ -1,0 +1,294 @@
+// Guard-band hidden layer: packed-FP32 simulation with an exact FP64 fallback
+// (default filter bank, constant refractory span FZ, N <= kGbMaxSteps).
+//
+// The reference simulates the 8,112 hidden LIF neurons in float64
+// (network.py:261-326, neurons.py:83-126).  k_hidden_res reproduces that bit
+// for bit on the FP64 pipe.  This kernel runs the same dynamics in float32,
+// two windows per lane packed into float2 registers (FFMA2/FADD2: half the
+// instructions and twice the pipe rate of FP64), and proves per window that
+// its spikes are the FP64 kernel's:
+//
+//   state  w = v - E_L >= 0 (so the LIF step is ONE fused multiply-add:
+//          w' = w D + beta I, D = 1 - beta g, with beta folded into the taps);
+//          reset / clamp / refractory as in the FP64 kernel (w = 0 <=> v = E_L);
+//   bound  while the two runs take the same spike decisions, the float32 and
+//          float64 trajectories differ by at most e(s) <= D e(s-1) + eps, eps =
+//          24 u beta S_w + 2.1 u (1.01 theta D + beta S_w) + 2^-50 (...),
+//          u = 2^-24, theta = V_T - E_L and S_w = max over features of
+//          sum_k |tap_{f,k}| max_s |c(s, level_k)| for THIS window (the table
+//          rounding, the 9-term float32 stencil, the constants' rounding and
+//          the one FFMA; the float64 side's own rounding in the 2^-50 term),
+//          so |e| <= e_max = eps / (1 - D);
+//   band   a live neuron with theta - delta <= w' < theta + delta, delta =
+//          2 e_max + 4 u theta, could take a different decision: the window
+//          is flagged.  Outside the band both runs decide alike, so by
+//          induction an unflagged window's spike raster IS the FP64 raster;
+//   redo   flagged windows (a few per cent) are re-simulated by k_hidden_fix
+//          with the FP64 step of k_hidden_res, overwriting their raster.
+//
+// The result is the bit-identical hidden raster of the FP64 kernel (tests:
+// test_hidden_kernel_variants_identical, the per-neuron counts of 1,000
+// reference images).
+#pragma once
+#include "hidden.cuh"
+
+namespace snn {
+
+constexpr int kGbWarps = 16;
+constexpr int kGbMaxSteps = 200;  // fp32 table [N][256] + [256] level maxima in <= 201 KB
+
+__host__ __device__ inline size_t gb_smem_bytes(int N) { return ((size_t)N + 1) * 256 * sizeof(float); }
+
+// Work list of flagged windows (indices in the batch's compacted window list).
+__device__ __forceinline__ void gb_flag(const BatchArgs &A, bool flag, int gw) {
+    const unsigned b = __ballot_sync(kFull, flag);
+    if (!b) return;
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == __ffs(b) - 1) base = atomicAdd(A.fix_count, __popc(b));
+    base = __shfl_sync(kFull, base, __ffs(b) - 1);
+    if (flag) A.fix_list[base + __popc(b & ((1u << lane) - 1u))] = gw;
+}
+
+// Stencil sums of the default bank for two windows at once (x: the 9 input
+// traces of window A in .x, of window B in .y): chain k-ordered like the FP64
+// kernel, zero taps skipped, taps pre-scaled by beta.
+template <int F>
+__device__ __forceinline__ float2 gb_current(const float2 (&x)[9], const float (&tau)[4]) {
+    float2 I = make_float2(0.f, 0.f);
+    bool first = true;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        if (def_coef(F, k) != 0) {
+            const float t = def_coef(F, k) < 0 ? -tau[def_tap_slot(F, k)] : tau[def_tap_slot(F, k)];
+            const float2 tt = make_float2(t, t);
+            I = first ? __fmul2_rn(x[k], tt) : __ffma2_rn(x[k], tt, I);
+            first = false;
+        }
+    }
+    return I;
+}
+
+// Per-window float64 error bound -> the flag band, as float32 bit patterns
+// [blo, blo + bw): theta - delta and the band width 2 delta.
+struct GbBand {
+    float lo;    // theta - delta
+    uint32_t bw; // bits of 2 delta (q = w' - lo: near <=> 0 <= q < 2 delta <=> (uint)bits(q) < bw)
+};
+
+__device__ __forceinline__ GbBand gb_band(const ItemState &it, const float *cmax, const snn_lif_t &p) {
+    double lv[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) lv[k] = (double)cmax[(it.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu];
+    double S = 0.0;
+#pragma unroll
+    for (int f = 0; f < kNF; ++f) {
+        if (f >= 4 && f < 8) continue;  // negations of 0-3: the same sums
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) s += fabs(def_tap(f, k)) * lv[k];
+        S = fmax(S, s);
+    }
+    S *= 1.0 + 0x1p-40;
+    const double u = 0x1p-24;
+    const double beta = p.beta, D = 1.0 - beta * p.g, theta = p.vt - p.el;
+    const double bS = beta * S;
+    const double eps = 24.0 * u * bS + 2.1 * u * (1.01 * theta * D + bS) +
+                       0x1p-50 * (fabs(p.el) + fabs(p.vt) + bS + 1.01 * theta);
+    const double emax = eps / (1.0 - D);
+    const double delta = 2.0 * emax + 4.0 * u * theta;
+    GbBand b;
+    b.lo = (float)(theta - delta);
+    b.bw = __float_as_uint((float)(2.0 * delta));
+    return b;
+}
+
+// The decisions of feature f for both windows (inline PTX: ptxas otherwise
+// materialises the frozen bits through predicate spills).  q = w' - (theta -
+// delta), qh = w' - (theta + delta); the sign bits of q and qh are shifted
+// into nf / nh ("not fired" below / above the band, feature f at bit f after
+// the 12 features are done, highest first).  w' is kept (clamped at 0) iff
+// the neuron is live (frozen bit f clear) and 0 <= w' < theta - delta, one
+// unsigned compare of the bit pattern against ul = bits(theta - delta).
+__device__ __forceinline__ void gb_decide(float2 wn, float2 q, float2 qh, unsigned Fa, unsigned Fb, unsigned bit,
+                                          uint32_t ula, uint32_t ulb, unsigned &nfa, unsigned &nfb, unsigned &nha,
+                                          unsigned &nhb, float2 &w) {
+    float wa, wb;
+    asm("{\n\t.reg .pred pa, pb, ka, kb;\n\t.reg .b32 ta, tb;\n\t"
+        "and.b32 ta, %6, %8;\n\t"
+        "and.b32 tb, %7, %8;\n\t"
+        "setp.ne.u32 pa, ta, 0;\n\t"
+        "setp.ne.u32 pb, tb, 0;\n\t"
+        "setp.lt.and.u32 ka, %9, %11, !pa;\n\t"
+        "setp.lt.and.u32 kb, %10, %12, !pb;\n\t"
+        "selp.b32 %0, %9, 0, ka;\n\t"
+        "selp.b32 %1, %10, 0, kb;\n\t"
+        "shf.l.clamp.b32 %2, %13, %2, 1;\n\t"
+        "shf.l.clamp.b32 %3, %14, %3, 1;\n\t"
+        "shf.l.clamp.b32 %4, %15, %4, 1;\n\t"
+        "shf.l.clamp.b32 %5, %16, %5, 1;\n\t}"
+        : "=r"(*reinterpret_cast<uint32_t *>(&wa)), "=r"(*reinterpret_cast<uint32_t *>(&wb)), "+r"(nfa), "+r"(nfb),
+          "+r"(nha), "+r"(nhb)
+        : "r"(Fa), "r"(Fb), "r"(bit), "r"(__float_as_uint(wn.x)), "r"(__float_as_uint(wn.y)), "r"(ula), "r"(ulb),
+          "r"(__float_as_uint(q.x)), "r"(__float_as_uint(q.y)), "r"(__float_as_uint(qh.x)),
+          "r"(__float_as_uint(qh.y)));
+    w = make_float2(wa, wb);
+}
+
+template <int FZ>
+__global__ void __launch_bounds__(kGbWarps * 32, 1) k_hidden_gb(const BatchArgs A) {
+    extern __shared__ __align__(16) float gtab[];  // [N][256] fp32 input traces, then [256] max |c| per level
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int N = A.c.n_steps;
+    const int nchunks = n_chunks(N);
+    float *cmax = gtab + (size_t)N * 256;
+    for (int i = tid; i < N * 256; i += kGbWarps * 32) gtab[i] = (float)__ldg(A.ctab + i);
+    if (tid < 256) {
+        double m = 0.0;
+        for (int s = 0; s < N; ++s) m = fmax(m, fabs(__ldg(A.ctab + (size_t)s * 256 + tid)));
+        cmax[tid] = (float)(m * (1.0 + 0x1p-20));  // rounded up
+    }
+    __syncthreads();
+    const snn_lif_t &p = A.c.lif_hid;
+    const float D = (float)(1.0 - p.beta * p.g);
+    const float2 D2 = make_float2(D, D);
+    float tau[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) tau[m] = (float)(p.beta * c_def_tap[m]);
+    const int groups = hidden_items(A, 1);          // groups of 32 windows
+    const int items = (groups + 1) >> 1;            // a lane takes window gw and gw + 32
+    const int stride = (int)gridDim.x * kGbWarps;
+    for (int item = warp * (int)gridDim.x + (int)blockIdx.x; item < items; item += stride) {
+        ItemState ia, ib;
+        window_setup(A, true, (2 * item) * kTile + lane, 0, nchunks, ia);
+        window_setup(A, 2 * item + 1 < groups, (2 * item + 1) * kTile + lane, 0, nchunks, ib);
+        const GbBand ba = gb_band(ia, cmax, p), bb = gb_band(ib, cmax, p);
+        const float2 lo2 = make_float2(-ba.lo, -bb.lo);
+        const float2 hi2 = make_float2(-(ba.lo + __uint_as_float(ba.bw)), -(bb.lo + __uint_as_float(bb.bw)));
+        const uint32_t ula = __float_as_uint(ba.lo), ulb = __float_as_uint(bb.lo);
+        uint32_t offa[9], offb[9];  // byte offsets of the 9 levels in a table row
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            offa[k] = ((ia.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu) * 4u;
+            offb[k] = ((ib.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu) * 4u;
+        }
+        float2 w[kNF];
+#pragma unroll
+        for (int f = 0; f < kNF; ++f) w[f] = make_float2(0.f, 0.f);
+        unsigned fza[FZ], fzb[FZ];
+#pragma unroll
+        for (int q = 0; q < FZ; ++q) fza[q] = fzb[q] = 0u;
+        bool near_a = false, near_b = false;
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int s0 = ch * kChunk;
+            const int nrows = min(kChunk, N - s0);
+            uint64_t pa0 = 0, pa1 = 0, pb0 = 0, pb1 = 0;
+#pragma unroll 1
+            for (int j = 0; j < nrows; ++j) {
+                const char *T = reinterpret_cast<const char *>(gtab + (size_t)(s0 + j) * 256);
+                float2 x[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k)
+                    x[k] = make_float2(*reinterpret_cast<const float *>(T + offa[k]),
+                                       *reinterpret_cast<const float *>(T + offb[k]));
+                unsigned Fa = 0, Fb = 0;
+#pragma unroll
+                for (int q = 0; q < FZ; ++q) {
+                    Fa |= fza[q];
+                    Fb |= fzb[q];
+                }
+                float2 I[kNF];
+                I[0] = gb_current<0>(x, tau);
+                I[1] = gb_current<1>(x, tau);
+                I[2] = gb_current<2>(x, tau);
+                I[3] = gb_current<3>(x, tau);
+#pragma unroll
+                for (int f = 4; f < 8; ++f) I[f] = make_float2(-I[f - 4].x, -I[f - 4].y);
+                I[8] = gb_current<8>(x, tau);
+                I[9] = gb_current<9>(x, tau);
+                I[10] = gb_current<10>(x, tau);
+                I[11] = gb_current<11>(x, tau);
+                unsigned nfa = 0, nfb = 0, nha = 0, nhb = 0;  // sign bits below / above the band
+#pragma unroll
+                for (int f = kNF - 1; f >= 0; --f) {
+                    const float2 wn = __ffma2_rn(w[f], D2, I[f]);
+                    gb_decide(wn, __fadd2_rn(wn, lo2), __fadd2_rn(wn, hi2), Fa, Fb, 1u << f, ula, ulb, nfa, nfb, nha,
+                              nhb, w[f]);
+                }
+                // near the threshold: at or above theta - delta, below theta + delta, live
+                near_a |= (~nfa & nha & ~Fa & 0xFFFu) != 0u;
+                near_b |= (~nfb & nhb & ~Fb & 0xFFFu) != 0u;
+                const unsigned ma = ~nfa & ~Fa & 0xFFFu, mb = ~nfb & ~Fb & 0xFFFu;
+#pragma unroll
+                for (int q = FZ - 1; q > 0; --q) {
+                    fza[q] = fza[q - 1];
+                    fzb[q] = fzb[q - 1];
+                }
+                fza[0] = ma;
+                fzb[0] = mb;
+                pa0 |= (uint64_t)(ma & 0x3Fu) << (8 * j);
+                pa1 |= (uint64_t)(ma >> kHalf) << (8 * j);
+                pb0 |= (uint64_t)(mb & 0x3Fu) << (8 * j);
+                pb1 |= (uint64_t)(mb >> kHalf) << (8 * j);
+            }
+            if (ia.on) {
+                uint64_t *dst = reinterpret_cast<uint64_t *>(ia.rout + (size_t)ch * ia.rstride);
+                dst[0] = pa0;
+                dst[kTile] = pa1;
+            }
+            if (ib.on) {
+                uint64_t *dst = reinterpret_cast<uint64_t *>(ib.rout + (size_t)ch * ib.rstride);
+                dst[0] = pb0;
+                dst[kTile] = pb1;
+            }
+        }
+        gb_flag(A, near_a && ia.on, (2 * item) * kTile + lane);
+        gb_flag(A, near_b && ib.on, (2 * item + 1) * kTile + lane);
+    }
+}
+
+// FP64 re-simulation of the flagged windows (the exact step of k_hidden_res,
+// table from global memory): one thread per window, its raster overwritten.
+template <bool SGN, int FZ>
+__global__ void __launch_bounds__(256) k_hidden_fix(const BatchArgs A) {
+    const int N = A.c.n_steps;
+    const int nchunks = n_chunks(N);
+    const int count = *A.fix_count;
+    const LifK ph = lif_k(A.c.lif_hid);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += gridDim.x * blockDim.x) {
+        ItemState it;
+        window_setup(A, true, A.fix_list[t], 0, nchunks, it);
+        double v[kNF];
+#pragma unroll
+        for (int f = 0; f < kNF; ++f) v[f] = A.c.lif_hid.el;
+        unsigned fz[FZ];
+#pragma unroll
+        for (int q = 0; q < FZ; ++q) fz[q] = 0u;
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int s0 = ch * kChunk, nrows = min(kChunk, N - s0);
+            uint64_t p0 = 0, p1 = 0;
+            for (int j = 0; j < nrows; ++j) {
+                const double *T = A.ctab + (size_t)(s0 + j) * 256;
+                double x[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) x[k] = __ldg(T + ((it.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu));
+                unsigned frozen = 0;
+#pragma unroll
+                for (int q = 0; q < FZ; ++q) frozen |= fz[q];
+                const unsigned m = hidden_step_def_fz<SGN>(ph, x, v, frozen);
+#pragma unroll
+                for (int q = FZ - 1; q > 0; --q) fz[q] = fz[q - 1];
+                fz[0] = m;
+                p0 |= (uint64_t)(m & 0x3Fu) << (8 * j);
+                p1 |= (uint64_t)(m >> kHalf) << (8 * j);
+            }
+            if (it.on) {
+                uint64_t *dst = reinterpret_cast<uint64_t *>(it.rout + (size_t)ch * it.rstride);
+                dst[0] = p0;
+                dst[kTile] = p1;
+            }
+        }
+    }
+}
+
+}  // namespace snn

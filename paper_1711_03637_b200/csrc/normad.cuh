@@ -45,6 +45,7 @@ struct TrainWS {
     uint16_t *step_k;   // [n][evcap] per step: active-list index of each spiking neuron, ascending
     double *norm;       // [n][N]     |d_hat(s)|
     double *wp;         // [n][22][N] per-warp partial sums of d_hat^2
+    int32_t *fix;       // [1 + n * 676] guard-band hidden layer: count, flagged windows
     int64_t evcap;
 };
 

@@ -33,6 +33,7 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#include "hidden_gb.cuh"
 #include "normad.cuh"
 
 namespace snn {

@@ -65,6 +65,7 @@ struct InferWS {
     uint8_t *raster;
     double *g;     // [n][N][10] G rows (k_gsum -> k_output)
     double *gabs;  // [n][N][10] sum of |W| rows (near-tie accounting only)
+    int32_t *fix;  // [1 + n * 676] guard-band hidden layer: count, flagged windows
 };
 
 size_t infer_ws_layout(const snn_consts_t *c, int64_t n, char *base, InferWS *w) {
@@ -83,6 +84,7 @@ size_t infer_ws_layout(const snn_consts_t *c, int64_t n, char *base, InferWS *w)
     x.raster = (uint8_t *)take(raster_bytes(c, n));
     x.g = (double *)take((size_t)n * c->n_steps * kNO * 8);
     x.gabs = (double *)take((size_t)n * c->n_steps * kNO * 8);
+    x.fix = (int32_t *)take(((size_t)n * kNPos + 1) * 4);
 
     if (w) *w = x;
     return off;
@@ -100,7 +102,7 @@ int64_t train_evcap(const snn_consts_t *c) {
 
 size_t train_ws_per_image(const snn_consts_t *c) {
     const size_t N = c->n_steps, cap = train_evcap(c);
-    return raster_bytes(c, 1) + kMaxTiles * kTile * 2 + 4 + 4 + 4 + kNH * 2 + (kNH + 1) * 4 + cap * 2 +
+    return raster_bytes(c, 1) + kNPos * 4 + kMaxTiles * kTile * 2 + 4 + 4 + 4 + kNH * 2 + (kNH + 1) * 4 + cap * 2 +
            (N + 1) * 4 + cap * 2 + N * 8 + kMaxTiles * N * 8 + 3 * (kCl + 1) * 4 + 8 + kCl * (N + 1) * 4 + 2 * cap * 2 +
            N * 8 + kNH * 2 * 2 + (kNH + kCl) * 4 + (size_t)kCl * kClRows * kNO * 8 / 64;
 }
@@ -135,6 +137,7 @@ size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base, 
     w.step_k = (uint16_t *)take(n * cap * 2);
     w.norm = (double *)take(n * N * 8);
     w.wp = (double *)take(n * kMaxTiles * N * 8);
+    w.fix = (int32_t *)take((n * kNPos + 1) * 4);
     w.evcap = (int64_t)cap;
     ShardWS x;
     memset(&x, 0, sizeof(x));  // flags (push, alias, skip) are set by the caller
@@ -191,6 +194,7 @@ int sm_count() {
 struct Knobs {
     int hid_ctas = 0;                  // k_hidden CTAs per SM (0 = occupancy limit); snn_set_pipeline
     int hid_res = 1;                   // snn_set_hidden_resident
+    int hid_gb = 1;                    // guard-band FP32 hidden kernel when it applies (snn_set_hidden_resident)
     int hid_fz = SNN_HID_FZ;           // -DSNN_HID_FZ=0: never the frozen-mask variant (A/B builds)
     int normad_cluster = 1;            // snn_set_normad_cluster
     long long *phase_clk = nullptr;    // snn_normad_phase_clocks
@@ -213,6 +217,29 @@ int refr_span(const snn_consts_t &c) {
     }
     return k;
 }
+// Guard-band FP32 hidden kernel + FP64 redo of the flagged windows
+// (hidden_gb.cuh): the same raster as k_hidden_res<.., FZ = 3>.
+template <bool SGN>
+int launch_hidden_gb(const BatchArgs &A, cudaStream_t st) {
+    static bool attr[kMaxDev] = {};
+    const int dev = cur_dev();
+    if (!attr[dev]) {
+        if (cudaFuncSetAttribute(k_hidden_gb<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)gb_smem_bytes(kGbMaxSteps)) != cudaSuccess)
+            return cuda_check("cudaFuncSetAttribute(k_hidden_gb)");
+        attr[dev] = true;
+    }
+    const int64_t items = ((int64_t)A.n_images * kMaxTiles + 1) / 2;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(sm_count(), items));
+    k_hidden_gb<3><<<grid, kGbWarps * 32, gb_smem_bytes(A.c.n_steps), st>>>(A);
+    int rc = cuda_check("k_hidden_gb");
+    if (rc) return rc;
+    k_hidden_fix<SGN, 3><<<(unsigned)(2 * sm_count()), 256, 0, st>>>(A);
+    if ((rc = cuda_check("k_hidden_fix"))) return rc;
+    if (A.out.hidden_redo) cudaMemcpyAsync(A.out.hidden_redo, A.fix_count, 4, cudaMemcpyDeviceToDevice, st);
+    return SNN_OK;
+}
+
 template <bool TRACE, bool DEF, bool SGN, int FZ>
 int launch_hidden_res(const BatchArgs &A, cudaStream_t st) {
     static bool attr[kMaxDev] = {};  // per device context (idempotent if two threads race)
@@ -257,7 +284,9 @@ int launch_hidden(const BatchArgs &A, cudaStream_t st) {
     if (g_ev_before) cudaEventRecord(g_ev_before, st);
     if (K.hid_res && A.c.n_steps <= kResMaxSteps) {  // table resident in shared memory
         if constexpr (DEF && !TRACE) {
-            if (K.hid_fz && refr_span(A.c) == 3) rc = launch_hidden_res<TRACE, DEF, SGN, 3>(A, st);
+            const bool fz3 = K.hid_fz && refr_span(A.c) == 3;
+            if (fz3 && K.hid_gb && A.fix_count && A.c.n_steps <= kGbMaxSteps) rc = launch_hidden_gb<SGN>(A, st);
+            else if (fz3) rc = launch_hidden_res<TRACE, DEF, SGN, 3>(A, st);
             else rc = launch_hidden_res<TRACE, DEF, SGN, 0>(A, st);
         } else {
             rc = launch_hidden_res<TRACE, DEF, SGN, 0>(A, st);
@@ -422,6 +451,8 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
     A.win_base = w.win_base;
     A.raster = out->raster ? out->raster : w.raster;
     A.gabs = w.gabs;
+    A.fix_count = w.fix;
+    A.fix_list = w.fix + 1;
 
     A.out = *out;
     const bool def = is_default_bank(*c);
@@ -472,6 +503,7 @@ extern "C" void snn_set_hidden_resident(int enable) {
     Knobs &K = knobs();
     K.hid_res = enable != 0;
     K.hid_fz = enable == 2 ? 0 : SNN_HID_FZ;
+    K.hid_gb = enable == 1;
 }
 
 extern "C" void snn_normad_phase_clocks(long long *d_clk) { knobs().phase_clk = d_clk; }
@@ -571,6 +603,8 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
         A.n_win = U.ws.n_win;
         A.win_base = U.ws.win_base;
         A.items_per_tile = is_default_bank(*c) ? 1 : 2;
+        A.fix_count = U.ws.fix;
+        A.fix_list = U.ws.fix + 1;
         int r;
         if ((r = is_default_bank(*c) ? launch_fast<true>(A, nullptr, st) : launch_fast<false>(A, nullptr, st)))
             return r;

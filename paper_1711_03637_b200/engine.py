@@ -170,6 +170,7 @@ class Engine:
                 out["out_raster"] = torch.empty((n, N), dtype=torch.int16, device=dev)
             if ties:
                 out["near_ties"] = torch.empty((n,), dtype=torch.int32, device=dev)
+            out["hidden_redo"] = torch.zeros((1,), dtype=torch.int32, device=dev)
             if trace:
                 out["ff"] = torch.empty((n, N, N_OUTPUTS), dtype=torch.float64, device=dev)
                 out["v_out"] = torch.empty((n, N, N_OUTPUTS), dtype=torch.float64, device=dev)
@@ -188,7 +189,7 @@ class Engine:
             ws = self.buffer("infer", ws_bytes)
             o = _native.InferOutC()
             for name, t in out.items():
-                whole = name in ("raster", "tile_base")
+                whole = name in ("raster", "tile_base", "hidden_redo")
                 setattr(o, name, t.data_ptr() if whole else t[i0:i0 + cn].data_ptr())
             _native.check(self.lib.snn_infer(
                 ctypes.byref(c), images[i0:i0 + cn].data_ptr(), cn, w.data_ptr(), ctab.data_ptr(),

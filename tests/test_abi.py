@@ -67,9 +67,10 @@ def test_struct_layout_matches_c(tmp_path):
 #include <stddef.h>
 #include "snn_b200.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(snn_consts_t), offsetof(snn_consts_t, lif_hid),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(snn_consts_t), offsetof(snn_consts_t, lif_hid),
          offsetof(snn_consts_t, inhibition), offsetof(snn_consts_t, taps), sizeof(snn_lif_t),
-         sizeof(snn_infer_out_t), offsetof(snn_infer_out_t, v_hid), offsetof(snn_infer_out_t, near_ties));
+         sizeof(snn_infer_out_t), offsetof(snn_infer_out_t, v_hid), offsetof(snn_infer_out_t, near_ties),
+         offsetof(snn_infer_out_t, hidden_redo));
   return 0;
 }
 ''')
@@ -79,7 +80,7 @@ int main(void) {
     C = _native.ConstsC
     want = [ctypes.sizeof(C), C.lif_hid.offset, C.inhibition.offset, C.taps.offset,
             ctypes.sizeof(_native.LifC), ctypes.sizeof(_native.InferOutC), _native.InferOutC.v_hid.offset,
-            _native.InferOutC.near_ties.offset]
+            _native.InferOutC.near_ties.offset, _native.InferOutC.hidden_redo.offset]
     assert got == want
 
 

@@ -399,7 +399,7 @@ def test_hidden_kernel_variants_identical(sd, cfg, bank, workloads, wfix):
     # and the ring kernel: same hidden raster and counts
     imgs = torch.from_numpy(workloads["c3_images"][:300].reshape(300, -1).copy()).to(eng.device)
     rast = []
-    for res in (1, 2, 0):
+    for res in (1, 3, 2, 0):
         eng.lib.snn_set_hidden_resident(res)
         try:
             o = eng.infer(c, imgs, w, raster=True)

@@ -228,3 +228,41 @@ def test_two_engines_one_process(sd, cfg, bank, workloads, wfix):
     for r in res:
         for x in r:
             assert np.array_equal(x, want)
+
+
+def test_guard_band_hidden_kernel_bit_identical(sd, cfg, bank, workloads, wfix):
+    """The guard-band hidden layer (float32 pairs + float64 redo of the flagged
+    windows, hidden_gb.cuh) against the float64 kernel (snn_set_hidden_resident
+    (3)): the compact hidden raster of all 10,000 config-3 images byte for
+    byte, the counts, a 100-image NormAD epoch bit for bit, and the redo
+    fraction reported by snn_infer_out_t.hidden_redo."""
+    from paper_1711_03637_b200.engine import get_engine, make_consts
+    eng, c = get_engine(), make_consts(cfg, bank)
+    n = len(workloads["c3_images"])
+    imgs = torch.from_numpy(workloads["c3_images"].reshape(n, -1).copy()).to(eng.device)
+    w = torch.from_numpy(wfix["w_fix"].copy()).to(eng.device)
+    res = {}
+    for mode in (1, 3):
+        eng.lib.snn_set_hidden_resident(mode)
+        try:
+            o = eng.infer(c, imgs, w, raster=True)
+            eng.stream.synchronize()
+            nb = int(o["tile_base"][n].item()) * (-(-c.n_steps // 8)) * 512
+            res[mode] = (o["raster"][:nb].cpu().numpy(), o["counts"].cpu().numpy(), int(o["hidden_redo"].item()))
+        finally:
+            eng.lib.snn_set_hidden_resident(1)
+    assert np.array_equal(res[1][0], res[3][0])
+    assert np.array_equal(res[1][1], res[3][1])
+    redo = res[1][2]
+    print(f"guard band: {redo} windows re-simulated in float64 (of 3,571,517 active)")
+    assert 0 < redo < 0.25 * 3_571_517
+    order = workloads["c2_order"][:100]
+    ims, labs = workloads["c2_images"][order], workloads["c2_labels"][order]
+    out = []
+    for mode in (1, 3):
+        eng.lib.snn_set_hidden_resident(mode)
+        try:
+            out.append(sd.train_epoch(ims, labs, sd.zero_weights(), bank, cfg, sd.LearnConfig())[0])
+        finally:
+            eng.lib.snn_set_hidden_resident(1)
+    assert np.array_equal(out[0], out[1])
