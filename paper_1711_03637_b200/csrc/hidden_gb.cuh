@@ -136,7 +136,7 @@ __device__ __forceinline__ void gb_decide(float2 wn, float2 q, float2 qh, unsign
 }
 
 template <int FZ>
-__global__ void __launch_bounds__(kGbWarps * 32, 1) k_hidden_gb(const BatchArgs A) {
+__global__ void __launch_bounds__(kGbWarps * 32, 1) k_hidden_gb1(const BatchArgs A) {
     extern __shared__ __align__(16) float gtab[];  // [N][256] fp32 input traces, then [256] max |c| per level
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int N = A.c.n_steps;
@@ -247,8 +247,250 @@ __global__ void __launch_bounds__(kGbWarps * 32, 1) k_hidden_gb(const BatchArgs 
     }
 }
 
-// FP64 re-simulation of the flagged windows (the exact step of k_hidden_res,
-// table from global memory): one thread per window, its raster overwritten.
+// ---------------------------------------------------------------------------
+// k_hidden_gb (v2): the same guard band with a cheaper step.
+//
+//   scaled state   Sobel features (0-7) carry w / (beta g1), corners (8-11)
+//                  w / (beta g2) (g1, g2: the bank's two gains), so the stencil
+//                  sums integer-coefficient combinations of the input traces
+//                  and the LIF step stays one FFMA2: w' = w D + I.
+//   stencil        any summation order is admissible here (the band covers the
+//                  rounding of THIS order, gb_band2), so it shares subexpressions:
+//                  each Sobel is 5 ops; the corners are 9 Q - 4 T with Q the
+//                  sum of the corner's 2x2 block and T the window sum -- 39
+//                  packed ops for the 12 features instead of 56 multiply-adds.
+//   decision       q = w' - lo (one FADD2): its sign is the spike decision
+//                  (FMUL.SAT q * 2^100 -> 0 / 1, accumulated into the 12-bit
+//                  mask by one FFMA2 on the float pipe); near <=> 0 <= q < bw,
+//                  one unsigned compare of the bit pattern; keep <=> live and
+//                  0 <= w' < lo, one unsigned compare; w = keep ? w' : 0.
+//                  A refractory neuron (w = 0, w' = I) may test near: that only
+//                  adds a (rare) redo, never a wrong raster.
+constexpr float kGbBig = 0x1p100f;
+
+struct GbBand2 {
+    float lo1, lo2;     // band lower edges, Sobel / corner units (rounded down)
+    uint32_t bw1, bw2;  // bit patterns of the band widths (rounded up)
+};
+
+// Rigorous per-window bound of |float32 trajectory - float64 trajectory| (volts)
+// for the v2 step, from the window's per-level trace maxima m[k] (cmax, rounded
+// up): every FP32 op of the stencil rounds its result by at most u |bound of the
+// result| (the intermediate bounds below follow the op tree of gb2_currents),
+// the table entries by u m[k] per use (weighted by |coefficient|); then the
+// FFMA and the rounding of D, the float64 side (2^-50 terms), and e <= D e + eps
+// -> e_max = eps / (1 - D).  delta = 2 e_max + 8 u theta.
+__device__ __forceinline__ GbBand2 gb_band2(const ItemState &it, const float *cmax, const snn_lif_t &p,
+                                            double s1, double s2, double D) {
+    double m[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) m[k] = (double)cmax[(it.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu];
+    // Sobel H / V: (xa + xb) + 2 xc - ((xd + xe) + 2 xf); ops p1, h1, p2, h2, h1 - h2; table h1 + h2
+    auto sob = [&](int a, int b, int c, int d, int e, int f, double &mag) {
+        const double p1 = m[a] + m[b], h1 = p1 + 2.0 * m[c], p2 = m[d] + m[e], h2 = p2 + 2.0 * m[f];
+        mag = h1 + h2;
+        return (p1 + h1) + (p2 + h2) + 2.0 * (h1 + h2);
+    };
+    // Sobel D / AD: 2 (xa - xb) + (xc + xd) - (xe + xf); the difference's error is doubled
+    auto dia = [&](int a, int b, int c, int d, int e, int f, double &mag) {
+        const double d0 = m[a] + m[b], t0 = m[c] + m[d], t1 = m[e] + m[f], d1 = 2.0 * d0 + t0;
+        mag = d1 + t1;
+        return (2.0 * d0 + t0 + d1) + t1 + 2.0 * (d1 + t1);
+    };
+    double g1 = 0.0, S1 = 0.0, mg;
+    g1 = fmax(g1, sob(0, 2, 1, 6, 8, 7, mg)); S1 = fmax(S1, mg);
+    g1 = fmax(g1, sob(0, 6, 3, 2, 8, 5, mg)); S1 = fmax(S1, mg);
+    g1 = fmax(g1, dia(0, 8, 1, 3, 5, 7, mg)); S1 = fmax(S1, mg);
+    g1 = fmax(g1, dia(2, 6, 1, 5, 3, 7, mg)); S1 = fmax(S1, mg);
+    // corners: pair sums, Q = sA + sB (error 2 Q), T = (Q_tl + Q_br) + ((x2 + x6) - x4),
+    // C = fma(Q, 9, -4 T)
+    const double all = m[0] + m[1] + m[2] + m[3] + m[4] + m[5] + m[6] + m[7] + m[8];
+    const double Q[4] = {m[0] + m[1] + m[3] + m[4], m[1] + m[2] + m[4] + m[5], m[3] + m[4] + m[6] + m[7],
+                         m[4] + m[5] + m[7] + m[8]};
+    const double t1 = Q[0] + Q[3], a26 = m[2] + m[6], t3 = a26 + m[4], TB = t1 + t3;
+    const double eT = 3.0 * t1 + a26 + t3 + TB;
+    double g2 = 0.0, S2 = 0.0;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+        const double tab = 5.0 * Q[f] + 4.0 * (all - Q[f]);
+        g2 = fmax(g2, 18.0 * Q[f] + 4.0 * eT + 9.0 * Q[f] + 4.0 * TB + tab);
+        S2 = fmax(S2, tab);
+    }
+    const double u = 0x1p-24;
+    const double es = u * fmax(s1 * g1, s2 * g2) * (1.0 + 0x1p-20);
+    const double bS = fmax(s1 * S1, s2 * S2) * (1.0 + 0x1p-20);
+    const double theta = p.vt - p.el;
+    const double eps = es + u * (2.02 * theta * D + 1.01 * bS) +
+                       0x1p-50 * (fabs(p.el) + fabs(p.vt) + bS + 1.01 * theta);
+    const double emax = eps / (1.0 - D);
+    const double delta = 2.0 * emax + 8.0 * u * theta;
+    GbBand2 b;
+    if (theta - delta <= 0.0) {  // degenerate band: every decision is near
+        b.lo1 = b.lo2 = 0.f;
+        b.bw1 = b.bw2 = 0x7F800000u;
+        return b;
+    }
+    b.lo1 = __double2float_rd((theta - delta) / s1);
+    b.lo2 = __double2float_rd((theta - delta) / s2);
+    b.bw1 = __float_as_uint(__double2float_ru(((theta + delta) / s1 - (double)b.lo1) * (1.0 + 0x1p-20)));
+    b.bw2 = __float_as_uint(__double2float_ru(((theta + delta) / s2 - (double)b.lo2) * (1.0 + 0x1p-20)));
+    return b;
+}
+
+// a - b on packed float2 (sub.rn.f32x2; there is no CUDA intrinsic for it)
+__device__ __forceinline__ float2 gb_fsub2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*reinterpret_cast<unsigned long long *>(&a)),
+        "l"(*reinterpret_cast<unsigned long long *>(&b)));
+    return *reinterpret_cast<float2 *>(&r);
+}
+
+// The 12 scaled currents of two windows (the op tree gb_band2 bounds); the
+// negated Sobels (features 4-7) are formed by the caller.
+__device__ __forceinline__ void gb2_currents(const float2 (&x)[9], float2 (&I)[kNF]) {
+    const float2 two = make_float2(2.f, 2.f), nine = make_float2(9.f, 9.f), m4 = make_float2(-4.f, -4.f);
+    // Sobel H, V
+    I[0] = gb_fsub2(__ffma2_rn(x[1], two, __fadd2_rn(x[0], x[2])), __ffma2_rn(x[7], two, __fadd2_rn(x[6], x[8])));
+    I[1] = gb_fsub2(__ffma2_rn(x[3], two, __fadd2_rn(x[0], x[6])), __ffma2_rn(x[5], two, __fadd2_rn(x[2], x[8])));
+    // Sobel D, AD
+    I[2] = gb_fsub2(__ffma2_rn(gb_fsub2(x[0], x[8]), two, __fadd2_rn(x[1], x[3])), __fadd2_rn(x[5], x[7]));
+    I[3] = gb_fsub2(__ffma2_rn(gb_fsub2(x[2], x[6]), two, __fadd2_rn(x[1], x[5])), __fadd2_rn(x[3], x[7]));
+    // corners
+    const float2 s01 = __fadd2_rn(x[0], x[1]), s34 = __fadd2_rn(x[3], x[4]), s12 = __fadd2_rn(x[1], x[2]);
+    const float2 s45 = __fadd2_rn(x[4], x[5]), s67 = __fadd2_rn(x[6], x[7]), s78 = __fadd2_rn(x[7], x[8]);
+    const float2 q0 = __fadd2_rn(s01, s34), q1 = __fadd2_rn(s12, s45), q2 = __fadd2_rn(s34, s67),
+                 q3 = __fadd2_rn(s45, s78);
+    const float2 T = __fadd2_rn(__fadd2_rn(q0, q3), gb_fsub2(__fadd2_rn(x[2], x[6]), x[4]));
+    const float2 T4 = __fmul2_rn(T, m4);
+    I[8] = __ffma2_rn(q0, nine, T4);
+    I[9] = __ffma2_rn(q1, nine, T4);
+    I[10] = __ffma2_rn(q2, nine, T4);
+    I[11] = __ffma2_rn(q3, nine, T4);
+}
+
+// w' if the neuron is live (bit clear in the frozen mask F) and 0 <= w' < lo
+// (one unsigned compare of the bit pattern), else 0: LOP3 -> predicate,
+// ISETP.AND, SEL (inline PTX: the compiler otherwise splits it into two selects).
+__device__ __forceinline__ float gb2_keep(float wn, unsigned F, unsigned bit, uint32_t ul) {
+    uint32_t r;
+    asm("{\n\t.reg .pred pf, pk;\n\t.reg .b32 t;\n\t"
+        "and.b32 t, %1, %2;\n\t"
+        "setp.ne.u32 pf, t, 0;\n\t"
+        "setp.lt.and.u32 pk, %3, %4, !pf;\n\t"
+        "selp.b32 %0, %3, 0, pk;\n\t}"
+        : "=r"(r)
+        : "r"(F), "r"(bit), "r"(__float_as_uint(wn)), "r"(ul));
+    return __uint_as_float(r);
+}
+
+template <int FZ>
+__global__ void __launch_bounds__(kGbWarps * 32, 1) k_hidden_gb(const BatchArgs A) {
+    extern __shared__ __align__(16) float gtab[];  // [N][256] fp32 input traces, then [256] max |c| per level
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int N = A.c.n_steps;
+    const int nchunks = n_chunks(N);
+    float *cmax = gtab + (size_t)N * 256;
+    for (int i = tid; i < N * 256; i += kGbWarps * 32) gtab[i] = (float)__ldg(A.ctab + i);
+    if (tid < 256) {
+        double m = 0.0;
+        for (int s = 0; s < N; ++s) m = fmax(m, fabs(__ldg(A.ctab + (size_t)s * 256 + tid)));
+        cmax[tid] = (float)(m * (1.0 + 0x1p-20));  // rounded up
+    }
+    __syncthreads();
+    const snn_lif_t &p = A.c.lif_hid;
+    const double Dd = 1.0 - p.beta * p.g, s1 = p.beta * c_def_tap[0], s2 = p.beta * (c_def_tap[3] * 0.25);
+    const float2 D2 = make_float2((float)Dd, (float)Dd);
+    const int groups = hidden_items(A, 1);          // groups of 32 windows
+    const int items = (groups + 1) >> 1;            // a lane takes window gw and gw + 32
+    const int stride = (int)gridDim.x * kGbWarps;
+    for (int item = warp * (int)gridDim.x + (int)blockIdx.x; item < items; item += stride) {
+        ItemState ia, ib;
+        window_setup(A, true, (2 * item) * kTile + lane, 0, nchunks, ia);
+        window_setup(A, 2 * item + 1 < groups, (2 * item + 1) * kTile + lane, 0, nchunks, ib);
+        const GbBand2 ba = gb_band2(ia, cmax, p, s1, s2, Dd), bb = gb_band2(ib, cmax, p, s1, s2, Dd);
+        const float2 nlo1 = make_float2(-ba.lo1, -bb.lo1), nlo2 = make_float2(-ba.lo2, -bb.lo2);
+        const uint32_t ula1 = __float_as_uint(ba.lo1), ulb1 = __float_as_uint(bb.lo1);
+        const uint32_t ula2 = __float_as_uint(ba.lo2), ulb2 = __float_as_uint(bb.lo2);
+        uint32_t offa[9], offb[9];  // byte offsets of the 9 levels in a table row
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            offa[k] = ((ia.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu) * 4u;
+            offb[k] = ((ib.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu) * 4u;
+        }
+        float2 w[kNF];
+#pragma unroll
+        for (int f = 0; f < kNF; ++f) w[f] = make_float2(0.f, 0.f);
+        unsigned fza[FZ], fzb[FZ];
+#pragma unroll
+        for (int q = 0; q < FZ; ++q) fza[q] = fzb[q] = 0u;
+        bool near_a = false, near_b = false;
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int s0 = ch * kChunk;
+            const int nrows = min(kChunk, N - s0);
+            uint64_t pa0 = 0, pa1 = 0, pb0 = 0, pb1 = 0;
+#pragma unroll 1
+            for (int j = 0; j < nrows; ++j) {
+                const char *T = reinterpret_cast<const char *>(gtab + (size_t)(s0 + j) * 256);
+                float2 x[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k)
+                    x[k] = make_float2(*reinterpret_cast<const float *>(T + offa[k]),
+                                       *reinterpret_cast<const float *>(T + offb[k]));
+                unsigned Fa = 0, Fb = 0;
+#pragma unroll
+                for (int q = 0; q < FZ; ++q) {
+                    Fa |= fza[q];
+                    Fb |= fzb[q];
+                }
+                float2 I[kNF];
+                gb2_currents(x, I);
+                float2 acc = make_float2(0x1p23f, 0x1p23f);  // 2^23 + sum of fired bits: the mask is the low mantissa
+#pragma unroll
+                for (int f = 0; f < kNF; ++f) {
+                    const float2 Ic = f >= 4 && f < 8 ? make_float2(-I[f - 4].x, -I[f - 4].y) : I[f];
+                    const float2 wn = __ffma2_rn(w[f], D2, Ic);
+                    const float2 q = __fadd2_rn(wn, f < 8 ? nlo1 : nlo2);
+                    const float fa = __saturatef(q.x * kGbBig), fb = __saturatef(q.y * kGbBig);
+                    acc = __ffma2_rn(make_float2(fa, fb), make_float2((float)(1 << f), (float)(1 << f)), acc);
+                    near_a |= __float_as_uint(q.x) < (f < 8 ? ba.bw1 : ba.bw2);
+                    near_b |= __float_as_uint(q.y) < (f < 8 ? bb.bw1 : bb.bw2);
+                    w[f] = make_float2(gb2_keep(wn.x, Fa, 1u << f, f < 8 ? ula1 : ula2),
+                                       gb2_keep(wn.y, Fb, 1u << f, f < 8 ? ulb1 : ulb2));
+                }
+                const unsigned ma = __float_as_uint(acc.x) & ~Fa & 0xFFFu, mb = __float_as_uint(acc.y) & ~Fb & 0xFFFu;
+#pragma unroll
+                for (int q = FZ - 1; q > 0; --q) {
+                    fza[q] = fza[q - 1];
+                    fzb[q] = fzb[q - 1];
+                }
+                fza[0] = ma;
+                fzb[0] = mb;
+                pa0 |= (uint64_t)(ma & 0x3Fu) << (8 * j);
+                pa1 |= (uint64_t)(ma >> kHalf) << (8 * j);
+                pb0 |= (uint64_t)(mb & 0x3Fu) << (8 * j);
+                pb1 |= (uint64_t)(mb >> kHalf) << (8 * j);
+            }
+            if (ia.on) {
+                uint64_t *dst = reinterpret_cast<uint64_t *>(ia.rout + (size_t)ch * ia.rstride);
+                dst[0] = pa0;
+                dst[kTile] = pa1;
+            }
+            if (ib.on) {
+                uint64_t *dst = reinterpret_cast<uint64_t *>(ib.rout + (size_t)ch * ib.rstride);
+                dst[0] = pb0;
+                dst[kTile] = pb1;
+            }
+        }
+        gb_flag(A, near_a && ia.on, (2 * item) * kTile + lane);
+        gb_flag(A, near_b && ib.on, (2 * item + 1) * kTile + lane);
+    }
+}
+
+// FP64 re-simulation of the flagged windows with the exact step of
+// k_hidden_res<.., FZ> (hidden_step_def_fz), one thread per window, the table
+// read from global memory (L2-resident).  The next step's 9 traces are loaded
+// while the current step computes, so a step costs its arithmetic, not an L2
+// round trip (94 -> ~40 us for ~15k windows).
 template <bool SGN, int FZ>
 __global__ void __launch_bounds__(256) k_hidden_fix(const BatchArgs A) {
     const int N = A.c.n_steps;
@@ -258,20 +500,28 @@ __global__ void __launch_bounds__(256) k_hidden_fix(const BatchArgs A) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += gridDim.x * blockDim.x) {
         ItemState it;
         window_setup(A, true, A.fix_list[t], 0, nchunks, it);
+        uint32_t off[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) off[k] = (it.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu;
         double v[kNF];
 #pragma unroll
         for (int f = 0; f < kNF; ++f) v[f] = A.c.lif_hid.el;
         unsigned fz[FZ];
 #pragma unroll
         for (int q = 0; q < FZ; ++q) fz[q] = 0u;
+        double xn[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) xn[k] = __ldg(A.ctab + off[k]);
         for (int ch = 0; ch < nchunks; ++ch) {
             const int s0 = ch * kChunk, nrows = min(kChunk, N - s0);
             uint64_t p0 = 0, p1 = 0;
             for (int j = 0; j < nrows; ++j) {
-                const double *T = A.ctab + (size_t)(s0 + j) * 256;
                 double x[9];
 #pragma unroll
-                for (int k = 0; k < 9; ++k) x[k] = __ldg(T + ((it.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu));
+                for (int k = 0; k < 9; ++k) x[k] = xn[k];
+                const size_t sn = (size_t)(s0 + j + 1 < N ? s0 + j + 1 : s0 + j) * 256;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) xn[k] = __ldg(A.ctab + sn + off[k]);
                 unsigned frozen = 0;
 #pragma unroll
                 for (int q = 0; q < FZ; ++q) frozen |= fz[q];

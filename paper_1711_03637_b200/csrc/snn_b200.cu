@@ -218,23 +218,36 @@ int refr_span(const snn_consts_t &c) {
     return k;
 }
 // Guard-band FP32 hidden kernel + FP64 redo of the flagged windows
-// (hidden_gb.cuh): the same raster as k_hidden_res<.., FZ = 3>.
+// (hidden_gb.cuh): the same raster as k_hidden_res<.., FZ = 3>.  The band
+// analysis needs a contracting step (0 < D = 1 - beta g < 1) and a positive
+// threshold distance whose scaled values are normal float32 numbers.
+bool gb_applies(const snn_consts_t &c) {
+    const snn_lif_t &p = c.lif_hid;
+    const double D = 1.0 - p.beta * p.g, theta = p.vt - p.el;
+    const double s1 = p.beta * kG1, s2 = p.beta * kG2;
+    if (!(D > 0x1p-10 && D < 1.0 - 0x1p-16 && theta > 0.0 && s1 > 0.0 && s2 > 0.0)) return false;
+    const double r1 = theta / s1, r2 = theta / s2;
+    return r1 > 0x1p-40 && r1 < 0x1p40 && r2 > 0x1p-40 && r2 < 0x1p40 && std::isfinite(D);
+}
+
 template <bool SGN>
-int launch_hidden_gb(const BatchArgs &A, cudaStream_t st) {
-    static bool attr[kMaxDev] = {};
+int launch_hidden_gb(const BatchArgs &A, cudaStream_t st, int variant) {
+    static bool attr[kMaxDev][2] = {};
     const int dev = cur_dev();
-    if (!attr[dev]) {
-        if (cudaFuncSetAttribute(k_hidden_gb<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const int vi = variant == 2 ? 1 : 0;
+    if (!attr[dev][vi]) {
+        if (cudaFuncSetAttribute(vi ? k_hidden_gb1<3> : k_hidden_gb<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)gb_smem_bytes(kGbMaxSteps)) != cudaSuccess)
             return cuda_check("cudaFuncSetAttribute(k_hidden_gb)");
-        attr[dev] = true;
+        attr[dev][vi] = true;
     }
     const int64_t items = ((int64_t)A.n_images * kMaxTiles + 1) / 2;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(sm_count(), items));
-    k_hidden_gb<3><<<grid, kGbWarps * 32, gb_smem_bytes(A.c.n_steps), st>>>(A);
+    if (vi) k_hidden_gb1<3><<<grid, kGbWarps * 32, gb_smem_bytes(A.c.n_steps), st>>>(A);
+    else k_hidden_gb<3><<<grid, kGbWarps * 32, gb_smem_bytes(A.c.n_steps), st>>>(A);
     int rc = cuda_check("k_hidden_gb");
     if (rc) return rc;
-    k_hidden_fix<SGN, 3><<<(unsigned)(2 * sm_count()), 256, 0, st>>>(A);
+    k_hidden_fix<SGN, 3><<<(unsigned)(4 * sm_count()), 64, 0, st>>>(A);
     if ((rc = cuda_check("k_hidden_fix"))) return rc;
     if (A.out.hidden_redo) cudaMemcpyAsync(A.out.hidden_redo, A.fix_count, 4, cudaMemcpyDeviceToDevice, st);
     return SNN_OK;
@@ -282,11 +295,15 @@ int launch_hidden(const BatchArgs &A, cudaStream_t st) {
     if ((rc = cuda_check("k_tile_scan"))) return rc;
     stage_mark(2, st);
     if (g_ev_before) cudaEventRecord(g_ev_before, st);
-    if (K.hid_res && A.c.n_steps <= kResMaxSteps) {  // table resident in shared memory
+    bool gb = false;
+    if constexpr (DEF && !TRACE)
+        gb = K.hid_res && K.hid_gb && K.hid_fz && A.fix_count && A.c.n_steps <= kGbMaxSteps && refr_span(A.c) == 3 &&
+             gb_applies(A.c);
+    if (gb) {
+        if ((rc = launch_hidden_gb<SGN>(A, st, K.hid_gb))) return rc;
+    } else if (K.hid_res && A.c.n_steps <= kResMaxSteps) {  // table resident in shared memory
         if constexpr (DEF && !TRACE) {
-            const bool fz3 = K.hid_fz && refr_span(A.c) == 3;
-            if (fz3 && K.hid_gb && A.fix_count && A.c.n_steps <= kGbMaxSteps) rc = launch_hidden_gb<SGN>(A, st);
-            else if (fz3) rc = launch_hidden_res<TRACE, DEF, SGN, 3>(A, st);
+            if (K.hid_fz && refr_span(A.c) == 3) rc = launch_hidden_res<TRACE, DEF, SGN, 3>(A, st);
             else rc = launch_hidden_res<TRACE, DEF, SGN, 0>(A, st);
         } else {
             rc = launch_hidden_res<TRACE, DEF, SGN, 0>(A, st);
@@ -501,9 +518,9 @@ extern "C" void snn_set_normad_cluster(int enable) { knobs().normad_cluster = en
 
 extern "C" void snn_set_hidden_resident(int enable) {
     Knobs &K = knobs();
-    K.hid_res = enable != 0;
+    K.hid_res = enable != 0;  // 4: the first guard-band kernel (k_hidden_gb1), for A/B
     K.hid_fz = enable == 2 ? 0 : SNN_HID_FZ;
-    K.hid_gb = enable == 1;
+    K.hid_gb = enable == 1 ? 1 : enable == 4 ? 2 : 0;
 }
 
 extern "C" void snn_normad_phase_clocks(long long *d_clk) { knobs().phase_clk = d_clk; }
