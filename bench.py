@@ -45,12 +45,20 @@ N_IMAGES = 10_000
 F_INF_PER_STEP = 389_516          # dense algorithmic flop per image-step
 F_TRAIN_PER_STEP = 592_316
 F_TRAIN_PER_IMAGE = 162_240
-# The roofline kernel of the default configuration and how its executed FP64
-# work per ACTIVE window-step is counted: from the SASS of the library that
-# runs (sass_loop_counts), the innermost loop (one window-step of 12 neurons):
-# flop = 2 DFMA + DMUL + DADD; FP64-pipe instructions = DFMA + DMUL + DADD + DSETP.
-HIDDEN_KERNEL = "_ZN3snn12k_hidden_resILb0ELb1ELb1ELi3EEEvNS_9BatchArgsE"   # k_hidden_res<0, 1, 1, 3>
-SASS_FALLBACK = {"DFMA": 50, "DMUL": 29, "DADD": 36, "DSETP": 6, "instructions": 235}  # r02 build, if cuobjdump is absent
+# The roofline kernel of the default configuration: the guard-band hidden
+# layer k_hidden_gb<3> (hidden_gb.cuh) -- float32 pairs whose
+# decisions are proven against the float64 trajectory, bound by the integer /
+# logic (ALU) pipe and instruction issue.  Its work per active window-step is
+# counted from the SASS of the library that runs (sass_loop_counts): the
+# innermost loop is one step of TWO windows per lane (64 per warp).
+HIDDEN_KERNEL = "_ZN3snn11k_hidden_gbILi3EEEvNS_9BatchArgsE"   # k_hidden_gb<3>
+# SASS opcodes that issue to the ALU pipe (integer / logic / compare / select)
+ALU_OPS = ("LOP3", "LOP", "SHF", "ISETP", "IMNMX", "VIMNMX", "SEL", "FSEL", "FSETP", "FMNMX", "IADD3", "VIADD",
+           "LEA", "PRMT", "PLOP3", "BMSK", "FLO", "BREV", "SGXT")
+FP32_FLOP = {"FFMA2": 4, "FADD2": 2, "FMUL2": 2, "FFMA": 2, "FADD": 1, "FMUL": 1}
+SASS_FALLBACK = {"instructions": 259, "alu": 130, "fp32_flop": 242, "fp32_instr": 99, "windows_per_iter": 64,
+                 "ops": {"ISETP": 47, "LOP3": 42, "FADD2": 40, "FFMA2": 34, "SEL": 28, "FMUL": 24, "LDS": 18,
+                         "SHF": 10}}  # r02 v2 build, if cuobjdump is absent
 LAUNCHES_PER_CHUNK = 5   # per sub-batch: k_prep, k_tile_scan, k_hidden, k_gsum, k_output
 PIPE_IMAGES = 0          # snn_set_pipeline sub-batch (library default: off)
 
@@ -60,9 +68,10 @@ def log(*a):
 
 
 def sass_loop_counts(so_path: str, fn: str) -> dict:
-    """FP64 op counts of the innermost loop of `fn` (the loop with the most
-    DFMA among the backward branches of the fewest instructions) in the SASS of
-    `so_path` (cuobjdump).  Falls back to SASS_FALLBACK (source: "fallback")."""
+    """Opcode counts of the innermost step loop of `fn` (the smallest backward-
+    branch loop with >= 20 FFMA2) in the SASS of `so_path` (cuobjdump): total
+    instructions, ALU-pipe instructions (ALU_OPS), FP32 flop (FFMA2 = 4 per
+    lane ...).  Falls back to SASS_FALLBACK (source: "fallback")."""
     import collections
     import re
     import shutil
@@ -85,9 +94,11 @@ def sass_loop_counts(so_path: str, fn: str) -> dict:
         body = [x for x in ins if int(m.group(1), 16) <= x[0] <= a]
         cnt = collections.Counter((tt.split()[1] if tt.startswith("@") else tt.split()[0]).split(".")[0]
                                   for _, tt in body)
-        if cnt["DFMA"] and (best is None or len(body) < best["instructions"]):
-            best = {"DFMA": cnt["DFMA"], "DMUL": cnt["DMUL"], "DADD": cnt["DADD"], "DSETP": cnt["DSETP"],
-                    "instructions": len(body)}
+        if cnt["FFMA2"] >= 20 and (best is None or len(body) < best["instructions"]):
+            best = {"instructions": len(body), "alu": sum(cnt[o] for o in ALU_OPS),
+                    "fp32_flop": sum(cnt[o] * f for o, f in FP32_FLOP.items()),
+                    "fp32_instr": sum(cnt[o] for o in FP32_FLOP), "windows_per_iter": 64,
+                    "ops": dict(cnt.most_common(12))}
     if best is None:
         return dict(SASS_FALLBACK, source="fallback (cuobjdump unavailable)")
     return dict(best, source=f"cuobjdump -sass -fun {fn} {os.path.basename(so_path)}")
@@ -201,15 +212,17 @@ class Clocks:
 
 
 def measure_peaks():
-    """FP64 DFMA / FP32 FFMA peaks of this GPU (libsnn_peaks.so microbenchmark)."""
+    """FP64 DFMA / FP32 FFMA (TFLOP/s) and ALU LOP3 (Tops, lane ops) peaks of
+    this GPU (libsnn_peaks.so microbenchmarks), best of 3."""
     from paper_1711_03637_b200.build import PEAKS_OUT
     lib = ctypes.CDLL(PEAKS_OUT)
-    f64, f32 = ctypes.c_double(), ctypes.c_double()
-    best64 = best32 = 0.0
+    f64, f32, alu = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    best64 = best32 = bestalu = 0.0
     for _ in range(3):
         lib.snn_measure_fma_peaks(ctypes.byref(f64), ctypes.byref(f32))
-        best64, best32 = max(best64, f64.value), max(best32, f32.value)
-    return best64, best32
+        lib.snn_measure_alu_peak(ctypes.byref(alu))
+        best64, best32, bestalu = max(best64, f64.value), max(best32, f32.value), max(bestalu, alu.value)
+    return best64, best32, bestalu
 
 
 def active_positions(images: np.ndarray) -> np.ndarray:
@@ -407,7 +420,9 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(near_ties, op=dist.ReduceOp.SUM)
     near_ties = near_ties.item()
-    ties_counts_same = bool(torch.equal(tie_out["counts"], eng.infer(c, d_img, d_w)["counts"]))
+    plain_out = eng.infer(c, d_img, d_w)
+    ties_counts_same = bool(torch.equal(tie_out["counts"], plain_out["counts"]))
+    hidden_redo = int(plain_out["hidden_redo"].item())
     hidden_frac = hidden_per_neuron_frac(eng, c, imgs_all, w_fix) if rank == 0 else None
 
     # ---- e2e: public API with host buffers (H2D images + weights, D2H counts)
@@ -426,20 +441,22 @@ def run_ours(args):
 
     line = None
     if rank == 0:
-        f64, f32 = measure_peaks()
+        f64, f32, alu_peak = measure_peaks()
         act = active_positions(shard.reshape(-1, 28, 28))
         n_steps = c.n_steps
         assert chunks_per_step == 1, "k_hidden events time one launch per step"
-        launch_ms = hk_ms                                    # k_hidden alone (CUDA events)
         call_ms = ker_ms / args.steps                        # whole (pipelined) snn_infer call
         from paper_1711_03637_b200 import _native
         sass = sass_loop_counts(_native.LIB_PATH, HIDDEN_KERNEL)
-        flop_ws = 2 * sass["DFMA"] + sass["DMUL"] + sass["DADD"]
-        pipe_ws = sass["DFMA"] + sass["DMUL"] + sass["DADD"] + sass["DSETP"]
-        exec_flop_launch = float(act.sum()) * n_steps * flop_ws
-        achieved = exec_flop_launch / (launch_ms * 1e-3) / 1e12
+        gb_ms = stage_ms.get("k_hidden_gb")
+        launch_ms = gb_ms if gb_ms else hk_ms                # k_hidden_gb alone (live CUDA events)
+        warp_steps = float(act.sum()) * n_steps / sass["windows_per_iter"]
+        alu_tops = warp_steps * sass["alu"] * 32 / (launch_ms * 1e-3) / 1e12
+        fp32_tflops = warp_steps * sass["fp32_flop"] * 32 / (launch_ms * 1e-3) / 1e12
+        clk_ghz = (clocks.get("sm_mhz") or 1965.0) / 1e3
+        issue_frac = warp_steps * sass["instructions"] / (launch_ms * 1e-3) / (4 * torch.cuda.get_device_properties(0).multi_processor_count * clk_ghz * 1e9)
         dense_tflops = (b - a) * F_INF_PER_STEP * n_steps / (ker_ms / args.steps * 1e-3) / 1e12
-        traffic_bytes, traffic_src = committed_traffic("k_hidden")
+        traffic_bytes, traffic_src = committed_traffic("k_hidden_gb")
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
@@ -448,34 +465,39 @@ def run_ours(args):
             "config": {"workload": "c3: batched inference, 10,000 synthetic MNIST-shaped 28x28 images, "
                                    "12x3x3 feature maps (8112 LIF) -> 10 LIF, T=100 ms, dt=1 ms",
                        "n_images": N_IMAGES, "t_ms": 100.0, "dt_ms": 1.0, "n_steps": n_steps,
-                       "parallelism": f"dp{world}", "collective": "one NCCL all_gather of int32 counts"
-                       if world > 1 else "none", "l2": "flushed between timed steps (256 MiB write)"},
+                       "parallelism": f"dp{world}", "collective": (f"one all_gather of int32 counts "
+                                                                    f"({dist.get_backend()})") if world > 1 else "none",
+                       "l2": "flushed between timed steps (256 MiB write)"},
             "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "api": "distributed.sharded_batch_counts (host numpy in/out)"},
             "gpu_launches": int(args.steps * launches_per_step),
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": f64, "unit": "TFLOP/s",
-                         "frac": achieved / f64, "traffic": traffic_bytes,
+            "roofline": {"bound": "alu", "achieved": alu_tops, "peak": alu_peak, "unit": "Tops (int32 lane ops)",
+                         "frac": alu_tops / alu_peak, "traffic": traffic_bytes,
                          "traffic_unit": "bytes per launch (DRAM read + write)", "traffic_source": traffic_src,
-                         "kernel": "k_hidden<DEF> (fused input-table gather + 3x3 stencil + hidden LIF, "
-                                   "spike raster out), timed alone with CUDA events (snn_profile_events)",
-                         "achieved_basis": f"executed fp64 flop: active windows ({int(act.sum())}) x N ({n_steps}) x "
-                                           f"{flop_ws} flop per window-step (2 x {sass['DFMA']} DFMA + "
-                                           f"{sass['DMUL']} DMUL + {sass['DADD']} DADD in the kernel's inner loop, "
+                         "kernel": "k_hidden_gb<3>: fused input-table gather + 3x3 stencil + hidden LIF in float32 "
+                                   "pairs with a per-window float64 error band (windows near a threshold decision "
+                                   "re-simulated in float64 by k_hidden_fix), spike raster out; timed alone with "
+                                   "the library's live CUDA events (snn_profile_stage_events)",
+                         "achieved_basis": f"ALU-pipe lane ops executed: active windows ({int(act.sum())}) x N "
+                                           f"({n_steps}) / {sass['windows_per_iter']} windows per warp-iteration x "
+                                           f"{sass['alu']} ALU instructions x 32 lanes (inner loop of "
+                                           f"{sass['instructions']} SASS instructions: {sass['ops']}; "
                                            f"{sass['source']})",
-                         "peak_source": "measured in this run: FP64 DFMA microbenchmark (libsnn_peaks.so); "
-                                        "MEASURED_PEAKS.json has no FP64 figure",
-                         "launch_ms": launch_ms, "call_ms": call_ms, "unpipelined_call_ms": call1_ms,
-                         "call_achieved_tflops": exec_flop_launch / (call_ms * 1e-3) / 1e12,
+                         "peak_source": "measured in this run: LOP3 throughput microbenchmark (libsnn_peaks.so); "
+                                        "MEASURED_PEAKS.json has no integer-pipe figure",
+                         "launch_ms": launch_ms, "hidden_layer_ms": hk_ms, "call_ms": call_ms,
+                         "unpipelined_call_ms": call1_ms,
+                         "issue_frac": issue_frac,
+                         "issue_basis": f"{sass['instructions']} SASS instructions per warp-iteration against 4 "
+                                        f"issue slots per SM per cycle at the sampled SM clock ({clk_ghz:.3f} GHz)",
+                         "fp32_tflops": fp32_tflops, "fp32_peak_tflops": f32, "fp32_frac": fp32_tflops / f32,
+                         "fp32_basis": f"{sass['fp32_flop']} FP32 flop per warp-iteration per lane "
+                                       f"({sass['fp32_instr']} FFMA2/FADD2/FMUL2/FMUL.SAT)",
+                         "fp64_peak_tflops": f64,
                          "dense_equiv_tflops": dense_tflops,
-                         "dense_equiv_basis": "SURVEY 8(d) F_inf = 389,516 flop per image-step",
-                         "fp32_peak_tflops": f32, "active_windows_per_image": float(act.mean()),
-                         "fp64_pipe_frac": achieved / flop_ws * pipe_ws / (f64 / 2),
-                         "fp64_pipe_basis": f"{pipe_ws} FP64-pipe instructions per active window-step "
-                                            f"({sass['DFMA']} DFMA + {sass['DMUL']} DMUL + {sass['DADD']} DADD + "
-                                            f"{sass['DSETP']} DSETP of {sass['instructions']} in the SASS of the inner "
-                                            "loop) against the DFMA instruction rate (peak / 2); ncu's "
-                                            "sm__pipe_fp64_cycles_active is the same quantity measured",
-                         "kernels": kernel_table(stage_ms, call1_ms, achieved / f64)},
+                         "dense_equiv_basis": "SURVEY 8(d) F_inf = 389,516 flop per image-step over the whole call",
+                         "active_windows_per_image": float(act.mean()),
+                         "kernels": kernel_table(stage_ms, call1_ms, alu_tops / alu_peak)},
             "clocks": clocks,
             "parity": {"c3_first200_counts_equal_reference": ref_prefix,
                        "c3_all10000_counts_equal_reference": ref_all,
@@ -486,7 +508,12 @@ def run_ours(args):
                        "output_near_ties_basis": "output steps within the rigorous rounding bound of the "
                                                  "reordered c_hidden @ W, all 10,000 c3 images (0 = counts "
                                                  "provably the reference's)",
-                       "counts_with_tie_detector_unchanged": ties_counts_same},
+                       "counts_with_tie_detector_unchanged": ties_counts_same,
+                       "hidden_redo_windows": hidden_redo,
+                       "hidden_redo_basis": "windows of the 10,000 images whose float32 trajectory came within "
+                                            "the error band of a threshold decision and were re-simulated in "
+                                            "float64 (k_hidden_fix); the raster is the float64 kernel's "
+                                            "bit for bit (tests/test_gpu_round2.py)"},
         }
     # ---- NormAD training (single GPU, rank 0)
     if rank == 0 and not args.skip_train:
@@ -533,24 +560,33 @@ def hidden_per_neuron_frac(eng, c, imgs_all, w):
 def stage_times(eng, c, d_img, d_w, flush, steps):
     """Per-kernel device time of a live un-pipelined snn_infer call: CUDA
     events the library records between its launches on its stream
-    (snn_profile_stage_events), L2 flushed before each call; medians."""
+    (snn_profile_stage_events; event 6 between the guard-band hidden kernel
+    and its float64 redo), L2 flushed before each call; medians."""
     import torch
-    names = ["k_prep", "k_tile_scan", "k_hidden_res", "k_gsum", "k_output"]
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
     for e in evs:
         e.record(eng.stream)   # created lazily on first record
-    arr = (ctypes.c_void_p * 6)(*[e.cuda_event for e in evs])
-    per = {k: [] for k in names}
+    arr = (ctypes.c_void_p * 7)(*[e.cuda_event for e in evs])
+    per = {}
     try:
         for _ in range(max(3, steps)):
             with torch.cuda.stream(eng.stream):
                 flush.zero_()
-            eng.lib.snn_profile_stage_events(arr, 6)
+            evs[6].record(eng.stream)  # stays before k_prep when no guard-band launch re-records it
+            eng.lib.snn_profile_stage_events(arr, 7)
             eng.infer(c, d_img, d_w)
             eng.lib.snn_profile_stage_events(None, 0)
-            evs[-1].synchronize()
-            for k, name in enumerate(names):
-                per[name].append(evs[k].elapsed_time(evs[k + 1]))
+            evs[5].synchronize()
+            t = [0.0] + [evs[0].elapsed_time(evs[k]) for k in range(1, 7)]
+            gb = t[6] > t[2]
+            st = {"k_prep": t[1], "k_tile_scan": t[2] - t[1]}
+            if gb:
+                st.update({"k_hidden_gb": t[6] - t[2], "k_hidden_fix": t[3] - t[6]})
+            else:
+                st["k_hidden_res"] = t[3] - t[2]
+            st.update({"k_gsum": t[4] - t[3], "k_output": t[5] - t[4]})
+            for k, v in st.items():
+                per.setdefault(k, []).append(v)
     finally:
         eng.lib.snn_profile_stage_events(None, 0)
     return {k: statistics.median(v) for k, v in per.items()}
@@ -583,6 +619,8 @@ def kernel_table(stage_ms, call_ms, hidden_frac):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm = float(mp.get("hbm_gbs", 6553.3))
     bounds = {"k_prep": "hbm/latency (one pass over the images)", "k_tile_scan": "latency (one CTA)",
+              "k_hidden_gb": "ALU pipe / issue (float32 pairs + integer decisions)",
+              "k_hidden_fix": "fp64 dependent chain per flagged window (latency)",
               "k_hidden_res": "fp64 pipe", "k_gsum": "issue / L2 gathers (W rows)",
               "k_output": "fp64 dependent chain per image (latency)"}
     out = {}
@@ -590,12 +628,15 @@ def kernel_table(stage_ms, call_ms, hidden_frac):
         e = {"ms": ms, "share_of_call": ms / call_ms if call_ms else None, "bound": bounds.get(k)}
         n = ncu.get(k)
         if n:
-            e["ncu"] = {x: n.get(x) for x in ("issue_active_pct", "fp64_pipe_pct", "dram_bytes", "duration_ms")}
+            e["ncu"] = {x: n.get(x) for x in ("issue_active_pct", "fp64_pipe_pct", "alu_pipe_pct", "fma_pipe_pct",
+                                              "dram_bytes", "duration_ms") if n.get(x) is not None}
             if n.get("dram_bytes"):
                 e["dram_frac_of_hbm_peak"] = n["dram_bytes"] / (ms * 1e-3) / 1e9 / hbm
-        if k == "k_hidden_res":
+        if k == "k_hidden_gb":
             e["frac"] = hidden_frac
-            e["frac_basis"] = "executed fp64 flop / FP64 DFMA peak (roofline.frac)"
+            e["frac_basis"] = "executed ALU-pipe lane ops / LOP3 peak (roofline.frac)"
+            if n and n.get("alu_pipe_pct") is not None:
+                e["ncu_alu_pipe_frac"] = n["alu_pipe_pct"] / 100.0
         elif k == "k_gsum" and n:
             e["frac"] = (n.get("issue_active_pct") or 0) / 100.0
             e["frac_basis"] = "issue slots busy (ncu smsp__issue_active); DRAM is dram_frac_of_hbm_peak"

@@ -134,7 +134,8 @@ void snn_profile_events(void *before, void *after);
 /* Profiling hook: with n_events >= 6 cudaEvent_t handles, every following
  * un-pipelined inference launch sequence records events[0] before k_prep,
  * [1] after k_prep, [2] after k_tile_scan, [3] after the hidden-layer kernel,
- * [4] after k_gsum and [5] after k_output on its stream, so the caller can
+ * [4] after k_gsum and [5] after k_output on its stream, and [6] (optional)
+ * between the guard-band hidden kernel and its float64 redo, so the caller can
  * time each kernel of a live call.  NULL / 0 disables. */
 void snn_profile_stage_events(void *const *events, int n_events);
 

@@ -51,6 +51,51 @@ extern "C" int snn_measure_fma_peaks(double *tflops_fp64, double *tflops_fp32) {
     return cudaGetLastError() == cudaSuccess ? 0 : 1002;
 }
 
+// ALU (integer / logic pipe) peak: independent LOP3 chains, 8 per thread, each
+// step one 3-input LOP3 (x = (x ^ a) & (x | b)); returns lane-ops per second
+// (x 1e12).  The guard-band hidden kernel is bound by this pipe.
+__global__ void __launch_bounds__(256) k_alu_peak(uint32_t *out, int iters, uint32_t a, uint32_t b) {
+    uint32_t x[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = threadIdx.x * 2654435761u + c;
+#pragma unroll 8
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            uint32_t y;
+            asm volatile("lop3.b32 %0, %1, %2, %3, 0x68;" : "=r"(y) : "r"(x[c]), "r"(a), "r"(b));
+            x[c] = y;
+        }
+    uint32_t s = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s ^= x[c];
+    if (s == 0x12345678u) out[0] = s;
+}
+
+extern "C" int snn_measure_alu_peak(double *tops) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint32_t *out;
+    cudaMalloc(&out, sizeof(uint32_t));
+    const int blocks = sms * 8, threads = 256, iters = 1 << 15;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_alu_peak<<<blocks, threads>>>(out, iters / 4, 0x5bd1e995u, 0x9e3779b9u);
+    cudaEventRecord(e0);
+    k_alu_peak<<<blocks, threads>>>(out, iters, 0x5bd1e995u, 0x9e3779b9u);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaFree(out);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *tops = 8.0 * (double)iters * blocks * threads / (ms * 1e-3) / 1e12;
+    return cudaGetLastError() == cudaSuccess ? 0 : 1002;
+}
+
 // Dependent-chain latency of one FP64 add/mul (cycles), single thread.
 __global__ void k_dp_latency(double *out, long long *cycles, int iters, double a, double b) {
     double x = out[0];

@@ -159,7 +159,7 @@ size_t train_ws(const snn_consts_t *c, int64_t chunk, TrainWS *out, char *base, 
 }
 
 cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;  // snn_profile_events
-cudaEvent_t g_stage[6] = {};                               // snn_profile_stage_events
+cudaEvent_t g_stage[7] = {};  // snn_profile_stage_events (6: between the guard-band kernel and its redo)
 inline void stage_mark(int k, cudaStream_t st) {
     if (g_stage[k]) cudaEventRecord(g_stage[k], st);
 }
@@ -247,6 +247,7 @@ int launch_hidden_gb(const BatchArgs &A, cudaStream_t st, int variant) {
     else k_hidden_gb<3><<<grid, kGbWarps * 32, gb_smem_bytes(A.c.n_steps), st>>>(A);
     int rc = cuda_check("k_hidden_gb");
     if (rc) return rc;
+    stage_mark(6, st);
     k_hidden_fix<SGN, 3><<<(unsigned)(4 * sm_count()), 64, 0, st>>>(A);
     if ((rc = cuda_check("k_hidden_fix"))) return rc;
     if (A.out.hidden_redo) cudaMemcpyAsync(A.out.hidden_redo, A.fix_count, 4, cudaMemcpyDeviceToDevice, st);
@@ -419,7 +420,7 @@ extern "C" void snn_profile_events(void *before, void *after) {
     g_ev_after = (cudaEvent_t)after;
 }
 extern "C" void snn_profile_stage_events(void *const *events, int n_events) {
-    for (int k = 0; k < 6; ++k) g_stage[k] = (events && k < n_events) ? (cudaEvent_t)events[k] : nullptr;
+    for (int k = 0; k < 7; ++k) g_stage[k] = (events && k < n_events) ? (cudaEvent_t)events[k] : nullptr;
 }
 
 extern "C" const char *snn_last_error(void) { return g_err; }

@@ -24,6 +24,8 @@ METRICS = [
     ("gpu__time_duration.sum", "duration"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64 pipe active %"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe active %"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe active %"),
     ("sm__warps_active.avg.per_cycle_active", "warps active / SM"),
     ("smsp__warps_eligible.avg.per_cycle_active", "eligible warps / scheduler"),
     ("launch__registers_per_thread", "registers / thread"),
@@ -70,6 +72,8 @@ def summarize(rep, fh, traffic, kernels=None):
                    "duration_ms": get("gpu__time_duration.sum", dur_scale),
                    "issue_active_pct": get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                    "fp64_pipe_pct": get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                   "alu_pipe_pct": get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                   "fma_pipe_pct": get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
                    "warps_active_per_sm": get("sm__warps_active.avg.per_cycle_active"),
                    "registers": get("launch__registers_per_thread"),
                    "warp_instructions": get("smsp__inst_executed.sum")}
