@@ -9,7 +9,8 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_1711_03637_b200 import build as _build  # noqa: E402
-os.environ["SNN_B200_LIB"] = _build.build_profile()  # hooks are compiled only into the profile build
+if not os.environ.get("SNN_B200_LIB"):  # hooks are compiled only into the profile build
+    os.environ["SNN_B200_LIB"] = _build.build_profile()
 import paper_1711_03637_b200 as sd  # noqa: E402
 from paper_1711_03637_b200.engine import get_engine, make_consts  # noqa: E402
 
