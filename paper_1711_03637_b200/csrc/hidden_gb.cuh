@@ -486,57 +486,116 @@ __global__ void __launch_bounds__(kGbWarps * 32, 1) k_hidden_gb(const BatchArgs 
     }
 }
 
-// FP64 re-simulation of the flagged windows with the exact step of
-// k_hidden_res<.., FZ> (hidden_step_def_fz), one thread per window, the table
-// read from global memory (L2-resident).  The next step's 9 traces are loaded
-// while the current step computes, so a step costs its arithmetic, not an L2
-// round trip (94 -> ~40 us for ~15k windows).
+// Taps of the default bank per feature (def_tap), for k_hidden_fix's lanes.
+__constant__ double c_fix_tap[kNF][9] = {
+#define SNN_TAPROW(f) {def_tap(f, 0), def_tap(f, 1), def_tap(f, 2), def_tap(f, 3), def_tap(f, 4), def_tap(f, 5), \
+                       def_tap(f, 6), def_tap(f, 7), def_tap(f, 8)}
+    SNN_TAPROW(0), SNN_TAPROW(1), SNN_TAPROW(2), SNN_TAPROW(3), SNN_TAPROW(4), SNN_TAPROW(5),
+    SNN_TAPROW(6), SNN_TAPROW(7), SNN_TAPROW(8), SNN_TAPROW(9), SNN_TAPROW(10), SNN_TAPROW(11)
+#undef SNN_TAPROW
+};
+
+// One LIF step of a hidden neuron with the frozen-history refractory rule of
+// lif_update_fz (hidden.cuh): returns whether it spiked.
 template <bool SGN, int FZ>
-__global__ void __launch_bounds__(256) k_hidden_fix(const BatchArgs A) {
+__device__ __forceinline__ bool fix_lif(double I, double &v, unsigned &hist, const LifK &ph) {
+    double t = __dsub_rn(v, ph.el);
+    t = __dmul_rn(ph.g, t);
+    t = __dsub_rn(I, t);
+    t = __dmul_rn(ph.beta, t);
+    const double vn = __dadd_rn(v, t);
+    const bool frozen = hist != 0u;
+    const bool pa = frozen || (SGN ? __double_as_longlong(vn) >= ph.vt_bits : vn >= ph.vt);
+    v = (pa || vn < ph.el) ? ph.el : vn;
+    const bool fired = pa && !frozen;
+    hist = ((hist << 1) | (fired ? 1u : 0u)) & ((1u << FZ) - 1u);
+    return fired;
+}
+
+// FP64 re-simulation of the flagged windows with the exact step of
+// k_hidden_res<.., FZ> (hidden_step_def_fz).  A window's 12 neurons are
+// independent given its input traces, so four lanes share a window: lane g
+// runs Sobel g, its negation g + 4 and corner g + 8 (the full 9-tap dgemm
+// chain: a zero tap adds x * 0 exactly and fma(x, t, 0) = x * t, so the
+// currents equal def_current's up to the sign of a zero, which the LIF update
+// cannot see since v != 0); two shuffles OR the lanes' bits into the step's
+// 12-bit mask.  A CTA's 32 windows advance in lockstep, so the table rows of
+// the next 8-step chunk are copied into shared memory (cp.async, double
+// buffered) while the current chunk computes: a step costs one stencil + one
+// LIF, not an L2 round trip.
+constexpr int kFixThreads = 128;
+template <bool SGN, int FZ>
+__global__ void __launch_bounds__(kFixThreads) k_hidden_fix(const BatchArgs A) {
+    __shared__ __align__(16) double ftab[2][kChunk * 256];
     const int N = A.c.n_steps;
     const int nchunks = n_chunks(N);
     const int count = *A.fix_count;
     const LifK ph = lif_k(A.c.lif_hid);
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += gridDim.x * blockDim.x) {
+    const int g = threadIdx.x & 3;
+    double ts[9], tc[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        ts[k] = c_fix_tap[g][k];
+        tc[k] = c_fix_tap[8 + g][k];
+    }
+    // copy table rows [ch * 8, ch * 8 + 8) into buffer b (16-byte cp.async)
+    auto fetch = [&](int ch, int b) {
+        const int rows = min(kChunk, N - ch * kChunk);
+        const double *src = A.ctab + (size_t)ch * kChunk * 256;
+        for (int i = threadIdx.x; i < rows * 128; i += kFixThreads) {
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&ftab[b][2 * i]);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + 2 * i));
+        }
+        asm volatile("cp.async.commit_group;");
+    };
+    const int nthr = (int)(gridDim.x * kFixThreads);
+    for (int tb = (int)(blockIdx.x * kFixThreads); tb < 4 * count; tb += nthr) {  // CTA-uniform
+        const int t = (tb + (int)threadIdx.x) >> 2;  // this quad's window
+        const bool have = t < count;
         ItemState it;
-        window_setup(A, true, A.fix_list[t], 0, nchunks, it);
+        window_setup(A, have, have ? A.fix_list[t] : 0, 0, nchunks, it);
         uint32_t off[9];
 #pragma unroll
         for (int k = 0; k < 9; ++k) off[k] = (it.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-        double v[kNF];
-#pragma unroll
-        for (int f = 0; f < kNF; ++f) v[f] = A.c.lif_hid.el;
-        unsigned fz[FZ];
-#pragma unroll
-        for (int q = 0; q < FZ; ++q) fz[q] = 0u;
-        double xn[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) xn[k] = __ldg(A.ctab + off[k]);
+        double v0 = A.c.lif_hid.el, v1 = v0, v2 = v0;
+        unsigned h0 = 0, h1 = 0, h2 = 0;
+        __syncthreads();  // the previous pass is done with both buffers
+        fetch(0, 0);
         for (int ch = 0; ch < nchunks; ++ch) {
-            const int s0 = ch * kChunk, nrows = min(kChunk, N - s0);
+            if (ch + 1 < nchunks) {
+                fetch(ch + 1, (ch + 1) & 1);
+                asm volatile("cp.async.wait_group 1;");
+            } else {
+                asm volatile("cp.async.wait_group 0;");
+            }
+            __syncthreads();  // chunk ch is in buffer ch & 1
+            const double *T = ftab[ch & 1];
+            const int nrows = min(kChunk, N - ch * kChunk);
             uint64_t p0 = 0, p1 = 0;
             for (int j = 0; j < nrows; ++j) {
                 double x[9];
 #pragma unroll
-                for (int k = 0; k < 9; ++k) x[k] = xn[k];
-                const size_t sn = (size_t)(s0 + j + 1 < N ? s0 + j + 1 : s0 + j) * 256;
+                for (int k = 0; k < 9; ++k) x[k] = T[j * 256 + off[k]];
+                double Is = __dmul_rn(x[0], ts[0]), Ic = __dmul_rn(x[0], tc[0]);
 #pragma unroll
-                for (int k = 0; k < 9; ++k) xn[k] = __ldg(A.ctab + sn + off[k]);
-                unsigned frozen = 0;
-#pragma unroll
-                for (int q = 0; q < FZ; ++q) frozen |= fz[q];
-                const unsigned m = hidden_step_def_fz<SGN>(ph, x, v, frozen);
-#pragma unroll
-                for (int q = FZ - 1; q > 0; --q) fz[q] = fz[q - 1];
-                fz[0] = m;
+                for (int k = 1; k < 9; ++k) {
+                    Is = __fma_rn(x[k], ts[k], Is);
+                    Ic = __fma_rn(x[k], tc[k], Ic);
+                }
+                unsigned m = fix_lif<SGN, FZ>(Is, v0, h0, ph) ? 1u << g : 0u;
+                m |= fix_lif<SGN, FZ>(-Is, v1, h1, ph) ? 1u << (g + 4) : 0u;
+                m |= fix_lif<SGN, FZ>(Ic, v2, h2, ph) ? 1u << (g + 8) : 0u;
+                m |= __shfl_xor_sync(kFull, m, 1);
+                m |= __shfl_xor_sync(kFull, m, 2);
                 p0 |= (uint64_t)(m & 0x3Fu) << (8 * j);
                 p1 |= (uint64_t)(m >> kHalf) << (8 * j);
             }
-            if (it.on) {
+            if (g == 0 && have && it.on) {
                 uint64_t *dst = reinterpret_cast<uint64_t *>(it.rout + (size_t)ch * it.rstride);
                 dst[0] = p0;
                 dst[kTile] = p1;
             }
+            __syncthreads();  // everyone is done with buffer ch & 1 before it is refilled
         }
     }
 }

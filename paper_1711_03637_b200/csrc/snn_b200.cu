@@ -248,7 +248,7 @@ int launch_hidden_gb(const BatchArgs &A, cudaStream_t st, int variant) {
     int rc = cuda_check("k_hidden_gb");
     if (rc) return rc;
     stage_mark(6, st);
-    k_hidden_fix<SGN, 3><<<(unsigned)(4 * sm_count()), 64, 0, st>>>(A);
+    k_hidden_fix<SGN, 3><<<(unsigned)(4 * sm_count()), kFixThreads, 0, st>>>(A);
     if ((rc = cuda_check("k_hidden_fix"))) return rc;
     if (A.out.hidden_redo) cudaMemcpyAsync(A.out.hidden_redo, A.fix_count, 4, cudaMemcpyDeviceToDevice, st);
     return SNN_OK;
