@@ -165,8 +165,12 @@ void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_per_sm);
 void snn_set_hidden_resident(int enable);
 
 /* snn_train runs its sequential NormAD chain on a cluster of 8 CTAs that
- * keeps W in distributed shared memory (default, enable = 1) when N <= ~600,
- * else on one CTA; enable = 0 forces the one-CTA kernel (same results). */
+ * keeps W in distributed shared memory.  enable = 1 (default) or 3: the
+ * cluster kernel with the G partials pushed to the leader when its shared
+ * memory fits, else pulled (2 forces pulling), else one CTA (0 forces it);
+ * 4: the kernel whose output scan of image i+1 runs speculatively during
+ * image i's update and is proven or redone (normad_spec.cuh; experimental,
+ * slower so far).  All give the same weights (1-4 bit for bit). */
 void snn_set_normad_cluster(int enable);
 
 /* Profiling hook: when d_clk (device, int64 [64][16]) is set, the cluster
@@ -196,7 +200,9 @@ size_t snn_train_workspace(const snn_consts_t *c, int64_t n_images);
 /* Sequential online NormAD over n images in the given order, updating
  * d_weights in place (float64 [8112][10]).  d_counts: [n][10] pre-update
  * output counts.  d_status (int32[4], device): [0] status code, [1] index of
- * the failing image, [2] images completed.  On SNN_ENONFINITE the weights hold
+ * the failing image, [2] images completed, [3] output scans the speculative
+ * kernel had to redo on the exact sums (telemetry).
+ * On SNN_ENONFINITE the weights hold
  * the state before the failing image (the reference raises and discards it). */
 int snn_train(const snn_consts_t *c, const uint8_t *d_images, const uint8_t *d_labels,
               int64_t n_images, double *d_weights, const double *d_ctab, int32_t *d_counts,

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "snn_b200.cu")
 OUT = os.path.join(HERE, "libsnn_b200.so")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("snn_b200.cu", "hidden.cuh", "hidden_gb.cuh", "normad.cuh", "normad_cl.cuh",
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("snn_b200.cu", "hidden.cuh", "hidden_gb.cuh", "normad.cuh", "normad_cl.cuh", "normad_spec.cuh",
                                                  "snn_common.cuh", "preprocess.cuh")]
 DEPS.append(os.path.join(ROOT, "include", "snn_b200.h"))
 

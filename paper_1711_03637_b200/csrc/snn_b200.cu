@@ -7,6 +7,7 @@
 #include <mutex>
 
 #include "normad_cl.cuh"
+#include "normad_spec.cuh"
 #include "preprocess.cuh"
 
 using namespace snn;
@@ -561,14 +562,21 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     if (c->n_steps > 65535) return set_error(SNN_EINVAL, "training supports n_steps <= 65535");
     // the W-resident cluster kernel when its shared memory fits, else the one-CTA kernel
     const Knobs &K = knobs();
-    const bool cl_push = K.normad_cluster == 1 && normad_cl_smem_bytes(c->n_steps, true) <= 227 * 1024;
+    // mode 1 (default) / 3: the cluster kernel (partials pushed), 2: pulled;
+    // 4: the speculative-scan cluster kernel (normad_spec.cuh, experimental:
+    // bit-identical weights, slower so far -- DESIGN.md 4.1); 0: one CTA.
+    const size_t sp_smem = normad_spec_smem_bytes(c->n_steps);
+    const bool use_spec = K.normad_cluster == 4 && sp_smem <= 227 * 1024;
+    const bool cl_push = (K.normad_cluster == 1 || K.normad_cluster == 3) &&
+                         normad_cl_smem_bytes(c->n_steps, true) <= 227 * 1024;
     // long trials: sigma/R reuse the G array, so the cluster kernel fits up to N ~ 1,300
     const bool cl_alias = !cl_push && normad_cl_smem_bytes(c->n_steps, false) > 227 * 1024;
     const size_t cl_smem = normad_cl_smem_bytes(c->n_steps, cl_push, cl_alias);
     const bool use_cl = K.normad_cluster && cl_smem <= 227 * 1024;
     const NormadCaps caps = normad_caps(c);
     const size_t smem = normad_smem_bytes(c->n_steps, caps);
-    if (!use_cl && smem > 220 * 1024) return set_error(SNN_EINVAL, "n_steps too large for the sequential NormAD CTA");
+    if (!use_cl && !use_spec && smem > 220 * 1024)
+        return set_error(SNN_EINVAL, "n_steps too large for the sequential NormAD CTA");
     const int64_t chunk = train_chunk(c, n);
     TrainArgs T;
     memset(&T, 0, sizeof(T));
@@ -579,7 +587,11 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     SW.alias = cl_alias ? 1 : 0;
     SW.skip = K.normad_skip;
     if (!d_ws || ws_bytes < need) return set_error(SNN_ENOMEM, "workspace too small");
-    if (use_cl) {
+    if (use_spec) {
+        if (cudaFuncSetAttribute(k_normad_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem) !=
+            cudaSuccess)
+            return cuda_check("cudaFuncSetAttribute(k_normad_spec)");
+    } else if (use_cl) {
         if (cudaFuncSetAttribute(k_normad_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem) != cudaSuccess)
             return cuda_check("cudaFuncSetAttribute(k_normad_cl)");
     } else if (cudaFuncSetAttribute(k_normad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
@@ -632,13 +644,17 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
         U.counts = d_counts + i0 * kNO;
         k_compact<<<(unsigned)cn, kCThreads, 0, st>>>(U);
         if ((r = cuda_check("k_compact"))) return r;
-        if (use_cl) {
+        if (use_cl || use_spec) {
             k_shard<<<(unsigned)cn, kShThreads, k_shard_smem(c->n_steps), st>>>(U, Sb[b]);
             if ((r = cuda_check("k_shard"))) return r;
         }
         return SNN_OK;
     };
     auto normad = [&](int b, cudaStream_t st) -> int {
+        if (use_spec) {
+            k_normad_spec<<<kCl, kSpThreads, sp_smem, st>>>(Tb[b], Sb[b]);
+            return cuda_check("k_normad_spec");
+        }
         if (use_cl) {
             k_normad_cl<<<kCl, kClThreads, cl_smem, st>>>(Tb[b], Sb[b]);
             return cuda_check("k_normad_cl");

@@ -266,3 +266,33 @@ def test_guard_band_hidden_kernel_bit_identical(sd, cfg, bank, workloads, wfix):
         finally:
             eng.lib.snn_set_hidden_resident(1)
     assert np.array_equal(out[0], out[1])
+
+
+def test_speculative_normad_bit_identical(sd, cfg, bank, workloads):
+    """The speculative-scan NormAD kernel (snn_set_normad_cluster(4),
+    normad_spec.cuh) runs image i+1's output scan on the sums of the weights
+    before image i's update and proves it (or redoes it): its weights and
+    per-image counts equal the plain cluster kernel's bit for bit, and
+    d_status[3] counts the redone scans."""
+    from paper_1711_03637_b200.engine import get_engine, make_consts
+    eng = get_engine()
+    c = make_consts(cfg, bank, sd.LearnConfig())
+    n = 300
+    order = workloads["c2_order"][:n]
+    imgs = torch.from_numpy(workloads["c2_images"][order].reshape(n, -1).copy()).to(eng.device)
+    labs = torch.from_numpy(workloads["c2_labels"][order].astype(np.uint8)).to(eng.device)
+    res = {}
+    for mode in (3, 4):
+        eng.lib.snn_set_normad_cluster(mode)
+        try:
+            w = torch.zeros((8112, 10), dtype=torch.float64, device=eng.device)
+            cnt, status = eng.train(c, imgs, labs, w)
+            eng.stream.synchronize()
+            res[mode] = (w.cpu().numpy(), cnt.cpu().numpy(), status.cpu().numpy())
+        finally:
+            eng.lib.snn_set_normad_cluster(1)
+    assert np.array_equal(res[3][0], res[4][0])
+    assert np.array_equal(res[3][1], res[4][1])
+    assert res[4][2][0] == 0 and res[4][2][2] == n
+    print(f"speculative scans redone: {res[4][2][3]} of {n - 1}")
+    assert 0 <= res[4][2][3] < n
