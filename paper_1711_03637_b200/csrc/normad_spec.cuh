@@ -115,8 +115,13 @@ __device__ __forceinline__ bool outd_step_m(OutD &X, const snn_consts_t &c, doub
 // exact sequence of k_normad_cl's leader scan.  Writes the per-step spike
 // masks to om; returns this lane's count and (MARGIN) its smallest live
 // distance to the threshold.
+#ifdef SNN_SPEC_SCAN_NOINLINE
+#define SNN_SCAN_INLINE __noinline__
+#else
+#define SNN_SCAN_INLINE __forceinline__
+#endif
 template <bool MARGIN>
-__device__ __forceinline__ int spec_scan(const snn_consts_t &c, const double *G, uint16_t *om, int N,
+__device__ SNN_SCAN_INLINE int spec_scan(const snn_consts_t &c, const double *G, uint16_t *om, int N,
                                          double *M) {
     const int lane = threadIdx.x & 31;
     const int l = lane < kNO ? lane : kNO - 1;

@@ -9,6 +9,7 @@ import paper_1711_03637_b200 as sd  # noqa: E402
 from paper_1711_03637_b200.engine import get_engine, make_consts  # noqa: E402
 d = np.load(os.path.join(ROOT, "data", "workloads.npz"))
 eng = get_engine()
+eng.lib.snn_set_normad_cluster(4)  # the speculative kernel
 c = make_consts(sd.NetworkConfig(), sd.default_filter_bank(), sd.LearnConfig())
 order = d["c2_order"][:200]
 imgs = torch.from_numpy(d["c2_images"][order].reshape(len(order), -1).copy()).cuda()
