@@ -35,6 +35,7 @@
 namespace snn {
 
 constexpr int kGbWarps = 20;  // 5 per scheduler: 1.93 ms vs 2.03 (16), 2.03 (19), 2.13 (18), 2.15 (24) per 10k images
+constexpr int kGbWarpsSmall = 16;  // k_hidden_gb's other CTA size (the host picks the one with fewer wave-cycles)
 constexpr int kGbMaxSteps = 200;  // fp32 table [N][256] + [256] level maxima in <= 201 KB
 
 __host__ __device__ inline size_t gb_smem_bytes(int N) { return ((size_t)N + 1) * 256 * sizeof(float); }
@@ -383,14 +384,14 @@ __device__ __forceinline__ float gb2_keep(float wn, unsigned F, unsigned bit, ui
     return __uint_as_float(r);
 }
 
-template <int FZ>
-__global__ void __launch_bounds__(kGbWarps * 32, 1) k_hidden_gb(const BatchArgs A) {
+template <int FZ, int WARPS = kGbWarps>
+__global__ void __launch_bounds__(WARPS * 32, 1) k_hidden_gb(const BatchArgs A) {
     extern __shared__ __align__(16) float gtab[];  // [N][256] fp32 input traces, then [256] max |c| per level
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int N = A.c.n_steps;
     const int nchunks = n_chunks(N);
     float *cmax = gtab + (size_t)N * 256;
-    for (int i = tid; i < N * 256; i += kGbWarps * 32) gtab[i] = (float)__ldg(A.ctab + i);
+    for (int i = tid; i < N * 256; i += WARPS * 32) gtab[i] = (float)__ldg(A.ctab + i);
     if (tid < 256) {
         double m = 0.0;
         for (int s = 0; s < N; ++s) m = fmax(m, fabs(__ldg(A.ctab + (size_t)s * 256 + tid)));
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(kGbWarps * 32, 1) k_hidden_gb(const BatchArgs 
     const float2 D2 = make_float2((float)Dd, (float)Dd);
     const int groups = hidden_items(A, 1);          // groups of 32 windows
     const int items = (groups + 1) >> 1;            // a lane takes window gw and gw + 32
-    const int stride = (int)gridDim.x * kGbWarps;
+    const int stride = (int)gridDim.x * WARPS;
     for (int item = warp * (int)gridDim.x + (int)blockIdx.x; item < items; item += stride) {
         ItemState ia, ib;
         window_setup(A, true, (2 * item) * kTile + lane, 0, nchunks, ia);

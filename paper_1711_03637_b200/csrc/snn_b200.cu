@@ -233,19 +233,37 @@ bool gb_applies(const snn_consts_t &c) {
 
 template <bool SGN>
 int launch_hidden_gb(const BatchArgs &A, cudaStream_t st, int variant) {
-    static bool attr[kMaxDev][2] = {};
+    static bool attr[kMaxDev][3] = {};
     const int dev = cur_dev();
-    const int vi = variant == 2 ? 1 : 0;
+    const int64_t items = ((int64_t)A.n_images * kMaxTiles + 1) / 2;  // upper bound for the grid
+    // CTA size: each warp runs its items in waves over the SMs; with the
+    // measured per-item times of the two sizes (16 warps: 84.6 us, 20 warps:
+    // 101.6 us per wave at N = 100), take the one with the smaller
+    // ceil(items / slots) x wave time -- 20 warps for large batches, 16 when
+    // 20 would leave a mostly empty last wave (e.g. 1,250 images: 254 vs 305 us)
+    // (the active-window count is only known on the device; 357 per image is
+    // the MNIST-like average, and either size gives the same raster)
+    const int64_t est = (int64_t)A.n_images * 357 / 64 + 1;
+    const int64_t s16 = (int64_t)sm_count() * kGbWarpsSmall, s20 = (int64_t)sm_count() * kGbWarps;
+    const bool small = variant != 2 && ((est + s16 - 1) / s16) * 846 < ((est + s20 - 1) / s20) * 1016;
+    const int vi = variant == 2 ? 1 : small ? 2 : 0;
     if (!attr[dev][vi]) {
-        if (cudaFuncSetAttribute(vi ? k_hidden_gb1<3> : k_hidden_gb<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)gb_smem_bytes(kGbMaxSteps)) != cudaSuccess)
-            return cuda_check("cudaFuncSetAttribute(k_hidden_gb)");
+        cudaError_t e = vi == 1 ? cudaFuncSetAttribute(k_hidden_gb1<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)gb_smem_bytes(kGbMaxSteps))
+                        : vi == 2 ? cudaFuncSetAttribute(k_hidden_gb<3, kGbWarpsSmall>,
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)gb_smem_bytes(kGbMaxSteps))
+                                  : cudaFuncSetAttribute(k_hidden_gb<3, kGbWarps>,
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)gb_smem_bytes(kGbMaxSteps));
+        if (e != cudaSuccess) return cuda_check("cudaFuncSetAttribute(k_hidden_gb)");
         attr[dev][vi] = true;
     }
-    const int64_t items = ((int64_t)A.n_images * kMaxTiles + 1) / 2;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(sm_count(), items));
-    if (vi) k_hidden_gb1<3><<<grid, kGbWarps * 32, gb_smem_bytes(A.c.n_steps), st>>>(A);
-    else k_hidden_gb<3><<<grid, kGbWarps * 32, gb_smem_bytes(A.c.n_steps), st>>>(A);
+    const size_t smem = gb_smem_bytes(A.c.n_steps);
+    if (vi == 1) k_hidden_gb1<3><<<grid, kGbWarps * 32, smem, st>>>(A);
+    else if (vi == 2) k_hidden_gb<3, kGbWarpsSmall><<<grid, kGbWarpsSmall * 32, smem, st>>>(A);
+    else k_hidden_gb<3, kGbWarps><<<grid, kGbWarps * 32, smem, st>>>(A);
     int rc = cuda_check("k_hidden_gb");
     if (rc) return rc;
     stage_mark(6, st);
