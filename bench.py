@@ -728,6 +728,33 @@ def critical_path_model(c):
                      "(issue-bound single warp, scripts/scan_micro.py)"}
 
 
+def train_kernel_table():
+    """The training kernels' bounds and the fraction of each, from the newest
+    committed ncu capture (profiles/<round>_kernels.json): k_normad_cl is the
+    sequential chain (its fraction is the dependent-chain model over the
+    measured time per image, critical_path.frac_of_measured); k_compact and
+    k_shard are the W-independent preparation, overlapped with the chain on
+    an auxiliary stream (issue slots busy)."""
+    prof, src = committed_kernels()
+    out = {}
+    for name, recs in prof.items():
+        k = _short(name)
+        if k in ("k_compact", "k_shard", "k_normad_cl"):
+            r = recs[0]
+            e = {"ncu": {x: r.get(x) for x in ("duration_ms", "issue_active_pct", "fp64_pipe_pct", "alu_pipe_pct",
+                                              "dram_bytes") if r.get(x) is not None}}
+            if k == "k_normad_cl":
+                e["bound"] = "latency: one-warp output scan + adjoint recursion per image (8 of 148 SMs)"
+                e["frac_basis"] = "critical_path.frac_of_measured"
+            else:
+                e["bound"] = "issue / latency (per-image compaction, overlapped with the chain)"
+                e["frac"] = (r.get("issue_active_pct") or 0) / 100.0
+                e["frac_basis"] = "issue slots busy (ncu)"
+            out[k] = e
+    out["_source"] = src
+    return out
+
+
 def bench_train(args, sd, eng, d, cfg, bank):
     import torch
     from paper_1711_03637_b200.engine import make_consts
@@ -787,7 +814,9 @@ def bench_train(args, sd, eng, d, cfg, bank):
             "w_rel_err_vs_reference_epoch": rel, "train_errors": stats.n_errors,
             "dense_equiv_tflops": value * (F_TRAIN_PER_STEP * 100 + F_TRAIN_PER_IMAGE) / 1e12,
             "gpu_launches_per_epoch": 6 * train_chunks(eng, c, n),
-            "critical_path": critical_path_model(c),
+            "critical_path": dict(critical_path_model(c), frac_of_measured=critical_path_model(c)[
+                "model_us_per_image"] / (statistics.median(times) * 1e3 / n)),
+            "kernels": train_kernel_table(),
             "cpu_baseline": {"value": cpu, "unit": "images/s", "cores": 1, "kind": kind, "sample": desc}}
 
 
