@@ -159,7 +159,9 @@ void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_per_sm);
  * decision re-simulated in float64; otherwise the float64
  * kernel that keeps the whole input table in shared memory (one CTA of 20
  * warps per SM) when N <= 108, else the one that streams the table through a
- * ring.  enable = 3: the float64 table-resident kernel (frozen spike masks)
+ * ring.  The guard band is used for batches of >= 256 images (below that
+ * the float64 kernel is faster); enable = 5 uses it at any batch size.
+ * enable = 3: the float64 table-resident kernel (frozen spike masks)
  * instead of the guard-band kernel; enable = 2: float64 with per-neuron
  * refractory horizons; enable = 0: the float64 ring kernel. */
 void snn_set_hidden_resident(int enable);

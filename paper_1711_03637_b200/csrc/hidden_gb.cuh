@@ -37,6 +37,10 @@ namespace snn {
 constexpr int kGbWarps = 20;  // 5 per scheduler: 1.93 ms vs 2.03 (16), 2.03 (19), 2.13 (18), 2.15 (24) per 10k images
 constexpr int kGbWarpsSmall = 16;  // k_hidden_gb's other CTA size (the host picks the one with fewer wave-cycles)
 constexpr int kGbMaxSteps = 200;  // fp32 table [N][256] + [256] level maxima in <= 201 KB
+// Below this batch size the float64 kernel is faster (scripts/small_n.py: one
+// image 34 vs 64 us, 148 images 59 vs 87 us, crossover ~250): the guard band's
+// setup and its float64 redo launch (a 100-step serial chain) are fixed costs.
+constexpr int kGbMinImages = 256;
 
 __host__ __device__ inline size_t gb_smem_bytes(int N) { return ((size_t)N + 1) * 256 * sizeof(float); }
 
@@ -392,10 +396,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_hidden_gb(const BatchArgs A) 
     const int nchunks = n_chunks(N);
     float *cmax = gtab + (size_t)N * 256;
     for (int i = tid; i < N * 256; i += WARPS * 32) gtab[i] = (float)__ldg(A.ctab + i);
-    if (tid < 256) {
-        double m = 0.0;
-        for (int s = 0; s < N; ++s) m = fmax(m, fabs(__ldg(A.ctab + (size_t)s * 256 + tid)));
-        cmax[tid] = (float)(m * (1.0 + 0x1p-20));  // rounded up
+    __syncthreads();
+    if (tid < 256) {  // from the float table in shared memory (|float(c)| >= |c| (1 - 2^-24)), rounded up
+        float m = 0.f;
+        for (int s = 0; s < N; ++s) m = fmaxf(m, fabsf(gtab[s * 256 + tid]));
+        cmax[tid] = (float)((double)m * (1.0 + 0x1p-20));
     }
     __syncthreads();
     const snn_lif_t &p = A.c.lif_hid;

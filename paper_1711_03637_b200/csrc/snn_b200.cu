@@ -196,6 +196,7 @@ struct Knobs {
     int hid_ctas = 0;                  // k_hidden CTAs per SM (0 = occupancy limit); snn_set_pipeline
     int hid_res = 1;                   // snn_set_hidden_resident
     int hid_gb = 1;                    // guard-band FP32 hidden kernel when it applies (snn_set_hidden_resident)
+    int hid_gb_small = 0;              // ... also below kGbMinImages (snn_set_hidden_resident(5), tests)
     int hid_fz = SNN_HID_FZ;           // -DSNN_HID_FZ=0: never the frozen-mask variant (A/B builds)
     int normad_cluster = 1;            // snn_set_normad_cluster
     long long *phase_clk = nullptr;    // snn_normad_phase_clocks
@@ -318,7 +319,7 @@ int launch_hidden(const BatchArgs &A, cudaStream_t st) {
     bool gb = false;
     if constexpr (DEF && !TRACE)
         gb = K.hid_res && K.hid_gb && K.hid_fz && A.fix_count && A.c.n_steps <= kGbMaxSteps && refr_span(A.c) == 3 &&
-             gb_applies(A.c);
+             gb_applies(A.c) && (A.n_images >= kGbMinImages || K.hid_gb_small);
     if (gb) {
         if ((rc = launch_hidden_gb<SGN>(A, st, K.hid_gb))) return rc;
     } else if (K.hid_res && A.c.n_steps <= kResMaxSteps) {  // table resident in shared memory
@@ -540,7 +541,8 @@ extern "C" void snn_set_hidden_resident(int enable) {
     Knobs &K = knobs();
     K.hid_res = enable != 0;  // 4: the first guard-band kernel (k_hidden_gb1), for A/B
     K.hid_fz = enable == 2 ? 0 : SNN_HID_FZ;
-    K.hid_gb = enable == 1 ? 1 : enable == 4 ? 2 : 0;
+    K.hid_gb = enable == 1 || enable == 5 ? 1 : enable == 4 ? 2 : 0;
+    K.hid_gb_small = enable == 5;
 }
 
 extern "C" void snn_normad_phase_clocks(long long *d_clk) { knobs().phase_clk = d_clk; }

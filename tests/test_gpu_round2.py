@@ -259,7 +259,27 @@ def test_guard_band_hidden_kernel_bit_identical(sd, cfg, bank, workloads, wfix):
     order = workloads["c2_order"][:100]
     ims, labs = workloads["c2_images"][order], workloads["c2_labels"][order]
     out = []
-    for mode in (1, 3):
+    # small batches: the default takes the float64 kernel (no redo); mode 5
+    # forces the guard band there too -- same raster
+    small = imgs[:16]
+    o = eng.infer(c, small, w, raster=True)
+    eng.stream.synchronize()
+    assert int(o["hidden_redo"].item()) == 0
+    from paper_1711_03637_b200.api import decode_hidden
+    rs = []
+    for mode in (5, 3):  # decoded per image: raster bytes of padding lanes are never written
+        eng.lib.snn_set_hidden_resident(mode)
+        try:
+            o = eng.infer(c, small, w, raster=True)
+            eng.stream.synchronize()
+            r, tb, tp, nt = (o[k].cpu().numpy() for k in ("raster", "tile_base", "tile_pos", "n_tiles"))
+            rs.append((np.stack([decode_hidden(r, int(tb[i]), tp[i], int(nt[i]), c.n_steps) for i in range(16)]),
+                       o["counts"].cpu().numpy()))
+        finally:
+            eng.lib.snn_set_hidden_resident(1)
+    assert rs[0][0].any()
+    assert np.array_equal(rs[0][0], rs[1][0]) and np.array_equal(rs[0][1], rs[1][1])
+    for mode in (5, 3):  # 5: the guard band also for the 64-image first chunk
         eng.lib.snn_set_hidden_resident(mode)
         try:
             out.append(sd.train_epoch(ims, labs, sd.zero_weights(), bank, cfg, sd.LearnConfig())[0])
