@@ -59,7 +59,7 @@ FP32_FLOP = {"FFMA2": 4, "FADD2": 2, "FMUL2": 2, "FFMA": 2, "FADD": 1, "FMUL": 1
 SASS_FALLBACK = {"instructions": 259, "alu": 130, "fp32_flop": 242, "fp32_instr": 99, "windows_per_iter": 64,
                  "ops": {"ISETP": 47, "LOP3": 42, "FADD2": 40, "FFMA2": 34, "SEL": 28, "FMUL": 24, "LDS": 18,
                          "SHF": 10}}  # r02 v2 build, if cuobjdump is absent
-LAUNCHES_PER_CHUNK = 5   # per sub-batch: k_prep, k_tile_scan, k_hidden, k_gsum, k_output
+LAUNCHES_PER_CHUNK = 6   # per sub-batch: k_prep, k_tile_scan, k_hidden_gb, k_hidden_fix, k_gsum, k_output
 PIPE_IMAGES = 0          # snn_set_pipeline sub-batch (library default: off)
 
 
@@ -709,6 +709,17 @@ def train_chunks(eng, c, n):
     return 1 + -(-(n - first) // chunk)
 
 
+def train_launches(eng, c, n):
+    """Kernel launches of one snn_train call: per chunk k_prep, k_tile_scan,
+    the hidden layer (guard band + redo for chunks of >= 256 images, else the
+    float64 kernel), k_compact, k_shard, the NormAD kernel."""
+    chunk = int(eng.lib.snn_train_chunk(ctypes.byref(c), n))
+    sizes = [n] if n <= chunk else [min(chunk, 64)]
+    while sum(sizes) < n:
+        sizes.append(min(chunk, n - sum(sizes)))
+    return sum(7 if s >= 256 else 6 for s in sizes)
+
+
 def critical_path_model(c):
     """Per-image latency floor of the sequential NormAD chain:
     the output scan's dependent chain per step (no output spike: 6 FP64 ops
@@ -813,7 +824,7 @@ def bench_train(args, sd, eng, d, cfg, bank):
             "e2e": {"value": e2e, "unit": "images/s", "api": "train_epoch (host numpy in/out)"},
             "w_rel_err_vs_reference_epoch": rel, "train_errors": stats.n_errors,
             "dense_equiv_tflops": value * (F_TRAIN_PER_STEP * 100 + F_TRAIN_PER_IMAGE) / 1e12,
-            "gpu_launches_per_epoch": 6 * train_chunks(eng, c, n),
+            "gpu_launches_per_epoch": train_launches(eng, c, n),
             "critical_path": dict(critical_path_model(c), frac_of_measured=critical_path_model(c)[
                 "model_us_per_image"] / (statistics.median(times) * 1e3 / n)),
             "kernels": train_kernel_table(),
