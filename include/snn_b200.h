@@ -175,6 +175,12 @@ void snn_set_hidden_resident(int enable);
  * slower so far).  All give the same weights (1-4 bit for bit). */
 void snn_set_normad_cluster(int enable);
 
+/* The output layer of batches of >= 256 images uses the lane-distributed
+ * step (k_output_dist: each lane owns one inhibition trace; fewer FP64
+ * instructions, the kernel is FP64-throughput bound there); enable = 0 forces
+ * the replicated-trace step everywhere (same bits). */
+void snn_set_output_dist(int enable);
+
 /* Profiling hook: when d_clk (device, int64 [64][16]) is set, the cluster
  * NormAD kernel records clock64() at its phase boundaries for the first 64
  * images of each snn_train call (NULL disables).  Effective only in the

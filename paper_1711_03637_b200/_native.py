@@ -76,6 +76,7 @@ SIGNATURES = [
     ("snn_profile_stage_events", None, [_vp, ctypes.c_int]),
     ("snn_set_pipeline", None, [ctypes.c_int64, ctypes.c_int]),
     ("snn_set_normad_cluster", None, [ctypes.c_int]),
+    ("snn_set_output_dist", None, [ctypes.c_int]),
     ("snn_set_hidden_resident", None, [ctypes.c_int]),
     ("snn_normad_phase_clocks", None, [_vp]),
     ("snn_normad_skip", None, [ctypes.c_int]),

@@ -1134,4 +1134,180 @@ __global__ void __launch_bounds__(kOutWarps2 * 32) k_output(const BatchArgs A, c
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// k_output_dist: the same output layer with the lane-distributed step
+// (dist_step): lane q < 10 owns inhibition trace q and the warp speculates the
+// next step's inhibition sums through 512 B of shared memory per warp -- the
+// reference's operation sequences, bit-identical to out_step, with ~28 FP64
+// instructions per lane-step instead of ~64.  On the serial chain of ONE warp
+// it is slower than out_step (263 vs 232 cycles per step,
+// scripts/scan_micro.py), but k_output over a large batch is bound by the
+// FP64 pipe (73% busy), so batches of >= 256 images take this kernel.
+// Each lane owns one trace; candidates are exchanged through shared memory:
+constexpr int kDistSpecHalf = 256;  // 15 x 16 B used; 512-aligned pair of buffers
+constexpr int kDistSpecBytes = 2 * kDistSpecHalf;
+
+struct DistState {
+    double Af, Bf;      // event-driven feed-forward recursions (slow, fast)
+    double al, bl;      // trace q times its decay, entering the next step
+    double ap, bp;      // al + 1, bl + 1
+    double c0, c1;      // own c for the next step: neuron q did not / did fire
+    double T;           // this lane's speculative inhibition sum for the next step
+    double v;
+    int live_from, cnt;
+    unsigned prev;      // output spikes of the previous step (10-bit)
+    unsigned cur;       // shared address of the buffer holding this step's candidates
+    unsigned rd[5];     // byte offsets of this lane's five pair loads
+    unsigned w0a, w0b, w1;  // byte offsets of the owner's c0 (twice) and c1 stores
+};
+
+__device__ __forceinline__ void sts64(unsigned a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ double lds64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ double2 lds128(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void dist_init(DistState &st, const snn_consts_t &c, char *spec, int lane) {
+    st.Af = st.Bf = 0.0;
+    st.al = st.bl = 0.0;
+    st.ap = st.bp = 1.0;
+    st.c0 = st.c1 = 0.0;  // (0 + 1) - (0 + 1) == +0
+    st.T = 0.0;           // pairwise10 of ten +0 is +0
+    st.v = c.lif_out.el;
+    st.live_from = 0;
+    st.cnt = 0;
+    st.prev = 0u;
+    st.cur = (unsigned)__cvta_generic_to_shared(spec);
+    const int sub = (lane >= kNO && lane < 2 * kNO) ? lane - kNO : -1;
+#pragma unroll
+    for (int m = 0; m < 5; ++m)
+        st.rd[m] = 48u * m + ((sub >= 0 && (sub >> 1) == m) ? 16u * (1u + (sub & 1)) : 0u);
+    const unsigned q = lane < kNO ? lane : kNO - 1, m = q >> 1, odd = q & 1u;
+    st.w0a = lane < kNO ? 48u * m + 8u * odd : 240u;  // 240..255: scratch slot
+    st.w0b = lane < kNO ? 48u * m + (odd ? 16u : 32u) + 8u * odd : 240u;
+    st.w1 = lane < kNO ? 48u * m + (odd ? 32u : 16u) + 8u * odd : 240u;
+}
+
+// The output layer's constants, held in registers across the scan.
+struct DistK {
+    double lam1, lam2, inh, el, vt, g, beta, refr;
+};
+
+__device__ __forceinline__ DistK dist_k(const snn_consts_t &c) {
+    return DistK{c.decay_slow, c.decay_fast, c.inhibition, c.lif_out.el, c.lif_out.vt,
+                c.lif_out.g, c.lif_out.beta, c.lif_out.refr};
+}
+
+// Advances one step given G (sum of W rows of hidden neurons spiking now).
+// Returns whether this lane's output neuron l fired; *ff_out = c_hidden @ W.
+__device__ __forceinline__ bool dist_step(DistState &st, const DistK &k, double G, int s, int l, int lane,
+                                         double *ff_out) {
+    st.Af = __dadd_rn(__dmul_rn(st.Af, k.lam1), G);
+    st.Bf = __dadd_rn(__dmul_rn(st.Bf, k.lam2), G);
+    const double ff = __dsub_rn(st.Af, st.Bf);
+    const unsigned pv = st.prev;  // warp-uniform
+    const bool mine = (pv >> l) & 1u;
+    const double a = mine ? st.ap : st.al;
+    const double b = mine ? st.bp : st.bl;
+    const double co = mine ? st.c1 : st.c0;
+    // this step's inhibition sum
+    double S = st.T;
+    if (pv != 0u) {
+        if ((pv & (pv - 1u)) == 0u) {
+            S = __shfl_sync(kFull, st.T, 9 + __ffs((int)pv));
+        } else {
+            double x[kNO];
+#pragma unroll
+            for (int q = 0; q < kNO; ++q) {
+                const unsigned m = q >> 1, bit = (pv >> q) & 1u;
+                const unsigned off = (q & 1) ? (bit ? 48u * m + 40u : 48u * m + 8u) : (bit ? 48u * m + 16u : 48u * m);
+                x[q] = lds64(st.cur + off);
+            }
+            S = pairwise10(x);
+        }
+    }
+    // candidates for the next step: traces, stores, loads (consumed below)
+    st.al = __dmul_rn(a, k.lam1);
+    st.bl = __dmul_rn(b, k.lam2);
+    st.c0 = __dsub_rn(st.al, st.bl);
+    st.ap = __dadd_rn(st.al, 1.0);
+    st.bp = __dadd_rn(st.bl, 1.0);
+    st.c1 = __dsub_rn(st.ap, st.bp);
+    // the two buffers are kDistSpecHalf apart: flip to the other one
+    const unsigned nxt = (st.cur & 256u) ? st.cur - 256u : st.cur + 256u;
+    st.cur = nxt;
+    sts64(nxt + st.w0a, st.c0);  // lanes >= 10 write a scratch slot
+    sts64(nxt + st.w0b, st.c0);
+    sts64(nxt + st.w1, st.c1);
+    __syncwarp();
+    double x[kNO];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+        const double2 p = lds128(nxt + st.rd[m]);
+        x[2 * m] = p.x;
+        x[2 * m + 1] = p.y;
+    }
+    // this step's drive and LIF (neurons.py:113-126); a refractory neuron holds v == E_L
+    const double drive = __dadd_rn(ff, __dmul_rn(k.inh, __dsub_rn(S, co)));
+    double t = __dsub_rn(st.v, k.el);
+    t = __dmul_rn(k.g, t);
+    t = __dsub_rn(drive, t);
+    t = __dmul_rn(k.beta, t);
+    const double vn = __dadd_rn(st.v, t);
+    const bool live = s >= st.live_from;
+    const bool fired = live && vn >= k.vt;
+    st.v = (!live || fired || vn < k.el) ? k.el : vn;
+    if (fired) st.live_from = next_live_step(s, k.refr);
+    st.prev = __ballot_sync(kFull, fired) & 0x3FFu;
+    st.cnt += fired ? 1 : 0;
+    // the next step's speculative sum
+    st.T = pairwise10(x);
+    *ff_out = ff;
+    return fired;
+}
+
+
+
+constexpr int kOutDistMinImages = 256;
+__global__ void __launch_bounds__(kOutWarps2 * 32) k_output_dist(const BatchArgs A, const double *G) {
+    __shared__ __align__(16) double s_g[kOutWarps2][kOSteps * kNO];
+    __shared__ __align__(512) char spec[kOutWarps2][kDistSpecBytes];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t img = (int64_t)blockIdx.x * kOutWarps2 + warp;
+    if (img >= A.n_images) return;
+    const int N = A.c.n_steps;
+    const int l = lane < kNO ? lane : kNO - 1;
+    const double *Gi = G + (size_t)img * N * kNO;
+    double *sg = s_g[warp];
+    DistState st;
+    dist_init(st, A.c, spec[warp], lane);
+    const DistK k = dist_k(A.c);
+    for (int s0 = 0; s0 < N; s0 += kOSteps) {
+        const int ns = min(kOSteps, N - s0);
+        for (int q = lane; q < ns * kNO; q += 32) sg[q] = __ldcs(Gi + (size_t)s0 * kNO + q);
+        __syncwarp();
+        for (int j = 0; j < ns; ++j) {
+            const int s = s0 + j;
+            double ff;
+            dist_step(st, k, sg[j * kNO + l], s, l, lane, &ff);
+            if (A.out.out_raster && lane == 0) A.out.out_raster[(size_t)img * N + s] = (uint16_t)st.prev;
+            if (lane < kNO) {
+                if (A.out.ff) A.out.ff[((size_t)img * N + s) * kNO + lane] = ff;
+                if (A.out.v_out) A.out.v_out[((size_t)img * N + s) * kNO + lane] = st.v;
+            }
+        }
+        __syncwarp();
+    }
+    if (lane < kNO) A.out.counts[(size_t)img * kNO + lane] = st.cnt;
+}
+
 }  // namespace snn

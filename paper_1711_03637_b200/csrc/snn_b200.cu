@@ -197,6 +197,7 @@ struct Knobs {
     int hid_res = 1;                   // snn_set_hidden_resident
     int hid_gb = 1;                    // guard-band FP32 hidden kernel when it applies (snn_set_hidden_resident)
     int hid_gb_small = 0;              // ... also below kGbMinImages (snn_set_hidden_resident(5), tests)
+    int out_dist = 1;                  // k_output_dist for large batches (snn_set_output_dist)
     int hid_fz = SNN_HID_FZ;           // -DSNN_HID_FZ=0: never the frozen-mask variant (A/B builds)
     int normad_cluster = 1;            // snn_set_normad_cluster
     long long *phase_clk = nullptr;    // snn_normad_phase_clocks
@@ -353,7 +354,11 @@ int launch_contract(const BatchArgs &A, double *g, cudaStream_t st) {
     else k_gsum<false><<<gg, kGWarps * 32, 0, st>>>(A, g, nullptr);
     if ((rc = cuda_check("k_gsum"))) return rc;
     stage_mark(4, st);
+    // large batches: the lane-distributed step (fewer FP64 instructions; the
+    // kernel is FP64-throughput bound there), small ones: the replicated step
+    // (shorter serial chain per image)
     if (gabs) k_output<true><<<og, kOutWarps2 * 32, 0, st>>>(A, g, gabs);
+    else if (A.n_images >= kOutDistMinImages && knobs().out_dist) k_output_dist<<<og, kOutWarps2 * 32, 0, st>>>(A, g);
     else k_output<false><<<og, kOutWarps2 * 32, 0, st>>>(A, g, nullptr);
     stage_mark(5, st);
     return cuda_check("k_output");
@@ -536,6 +541,7 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
 }
 
 extern "C" void snn_set_normad_cluster(int enable) { knobs().normad_cluster = enable; }
+extern "C" void snn_set_output_dist(int enable) { knobs().out_dist = enable; }
 
 extern "C" void snn_set_hidden_resident(int enable) {
     Knobs &K = knobs();
