@@ -429,7 +429,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_hidden_gb(const BatchArgs A) 
         unsigned fza[FZ], fzb[FZ];
 #pragma unroll
         for (int q = 0; q < FZ; ++q) fza[q] = fzb[q] = 0u;
-        bool near_a = false, near_b = false;
+        // smallest q bit pattern per window and feature class: near <=> min < bw
+        // (one unsigned min per neuron-step; negative q never counts)
+        uint32_t qa1 = 0xFFFFFFFFu, qa2 = 0xFFFFFFFFu, qb1 = 0xFFFFFFFFu, qb2 = 0xFFFFFFFFu;
         for (int ch = 0; ch < nchunks; ++ch) {
             const int s0 = ch * kChunk;
             const int nrows = min(kChunk, N - s0);
@@ -458,8 +460,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_hidden_gb(const BatchArgs A) 
                     const float2 q = __fadd2_rn(wn, f < 8 ? nlo1 : nlo2);
                     const float fa = __saturatef(q.x * kGbBig), fb = __saturatef(q.y * kGbBig);
                     acc = __ffma2_rn(make_float2(fa, fb), make_float2((float)(1 << f), (float)(1 << f)), acc);
-                    near_a |= __float_as_uint(q.x) < (f < 8 ? ba.bw1 : ba.bw2);
-                    near_b |= __float_as_uint(q.y) < (f < 8 ? bb.bw1 : bb.bw2);
+                    if (f < 8) {
+                        qa1 = min(qa1, __float_as_uint(q.x));
+                        qb1 = min(qb1, __float_as_uint(q.y));
+                    } else {
+                        qa2 = min(qa2, __float_as_uint(q.x));
+                        qb2 = min(qb2, __float_as_uint(q.y));
+                    }
                     w[f] = make_float2(gb2_keep(wn.x, Fa, 1u << f, f < 8 ? ula1 : ula2),
                                        gb2_keep(wn.y, Fb, 1u << f, f < 8 ? ulb1 : ulb2));
                 }
@@ -487,6 +494,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_hidden_gb(const BatchArgs A) 
                 dst[kTile] = pb1;
             }
         }
+        const bool near_a = qa1 < ba.bw1 || qa2 < ba.bw2, near_b = qb1 < bb.bw1 || qb2 < bb.bw2;
         gb_flag(A, near_a && ia.on, (2 * item) * kTile + lane);
         gb_flag(A, near_b && ib.on, (2 * item + 1) * kTile + lane);
     }
