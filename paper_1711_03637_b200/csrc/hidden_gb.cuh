@@ -296,17 +296,19 @@ __device__ __forceinline__ GbBand2 gb_band2(const ItemState &it, const float *cm
         mag = h1 + h2;
         return (p1 + h1) + (p2 + h2) + 2.0 * (h1 + h2);
     };
-    // Sobel D / AD: 2 (xa - xb) + (xc + xd) - (xe + xf); the difference's error is doubled
-    auto dia = [&](int a, int b, int c, int d, int e, int f, double &mag) {
-        const double d0 = m[a] + m[b], t0 = m[c] + m[d], t1 = m[e] + m[f], d1 = 2.0 * d0 + t0;
-        mag = d1 + t1;
-        return (2.0 * d0 + t0 + d1) + t1 + 2.0 * (d1 + t1);
-    };
-    double g1 = 0.0, S1 = 0.0, mg;
-    g1 = fmax(g1, sob(0, 2, 1, 6, 8, 7, mg)); S1 = fmax(S1, mg);
-    g1 = fmax(g1, sob(0, 6, 3, 2, 8, 5, mg)); S1 = fmax(S1, mg);
-    g1 = fmax(g1, dia(0, 8, 1, 3, 5, 7, mg)); S1 = fmax(S1, mg);
-    g1 = fmax(g1, dia(2, 6, 1, 5, 3, 7, mg)); S1 = fmax(S1, mg);
+    double g1 = 0.0, S1 = 0.0;
+    double mH, mV;
+    const double eH = sob(0, 2, 1, 6, 8, 7, mH), eV = sob(0, 6, 3, 2, 8, 5, mV);
+    g1 = fmax(eH, eV);
+    S1 = fmax(mH, mV);
+    // D = 0.5 (H + V) + (x0 - x8), AD = 0.5 (H - V) + (x2 - x6) (gb2_currents): half of
+    // H's and V's errors, the rounding of H +- V (bounded by |H| + |V|), the difference
+    // (its rounding and its two table entries: 2 (m_a + m_b)) and the FMA's rounding
+    const double mD = 2.0 * (m[0] + m[8]) + m[1] + m[3] + m[5] + m[7];
+    const double mAD = 2.0 * (m[2] + m[6]) + m[1] + m[5] + m[3] + m[7];
+    g1 = fmax(g1, 0.5 * (eH + eV + mH + mV) + 2.0 * (m[0] + m[8]) + mD);
+    g1 = fmax(g1, 0.5 * (eH + eV + mH + mV) + 2.0 * (m[2] + m[6]) + mAD);
+    S1 = fmax(S1, fmax(mD, mAD));
     // corners: pair sums, Q = sA + sB (error 2 Q), T = (Q_tl + Q_br) + ((x2 + x6) - x4),
     // C = fma(Q, 9, -4 T)
     const double all = m[0] + m[1] + m[2] + m[3] + m[4] + m[5] + m[6] + m[7] + m[8];
@@ -358,8 +360,10 @@ __device__ __forceinline__ void gb2_currents(const float2 (&x)[9], float2 (&I)[k
     I[0] = gb_fsub2(__ffma2_rn(x[1], two, __fadd2_rn(x[0], x[2])), __ffma2_rn(x[7], two, __fadd2_rn(x[6], x[8])));
     I[1] = gb_fsub2(__ffma2_rn(x[3], two, __fadd2_rn(x[0], x[6])), __ffma2_rn(x[5], two, __fadd2_rn(x[2], x[8])));
     // Sobel D, AD
-    I[2] = gb_fsub2(__ffma2_rn(gb_fsub2(x[0], x[8]), two, __fadd2_rn(x[1], x[3])), __fadd2_rn(x[5], x[7]));
-    I[3] = gb_fsub2(__ffma2_rn(gb_fsub2(x[2], x[6]), two, __fadd2_rn(x[1], x[5])), __fadd2_rn(x[3], x[7]));
+    // Sobel D, AD from H and V: D = 0.5 (H + V) + (x0 - x8), AD = 0.5 (H - V) + (x2 - x6)
+    const float2 half = make_float2(0.5f, 0.5f);
+    I[2] = __ffma2_rn(__fadd2_rn(I[0], I[1]), half, gb_fsub2(x[0], x[8]));
+    I[3] = __ffma2_rn(gb_fsub2(I[0], I[1]), half, gb_fsub2(x[2], x[6]));
     // corners
     const float2 s01 = __fadd2_rn(x[0], x[1]), s34 = __fadd2_rn(x[3], x[4]), s12 = __fadd2_rn(x[1], x[2]);
     const float2 s45 = __fadd2_rn(x[4], x[5]), s67 = __fadd2_rn(x[6], x[7]), s78 = __fadd2_rn(x[7], x[8]);
