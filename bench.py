@@ -626,7 +626,7 @@ def kernel_table(stage_ms, call_ms, hidden_frac):
     out = {}
     for k, ms in stage_ms.items():
         e = {"ms": ms, "share_of_call": ms / call_ms if call_ms else None, "bound": bounds.get(k)}
-        n = ncu.get(k)
+        n = ncu.get(k) or (ncu.get("k_output_dist") if k == "k_output" else None)
         if n:
             e["ncu"] = {x: n.get(x) for x in ("issue_active_pct", "fp64_pipe_pct", "alu_pipe_pct", "fma_pipe_pct",
                                               "dram_bytes", "duration_ms") if n.get(x) is not None}
