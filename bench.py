@@ -51,14 +51,14 @@ F_TRAIN_PER_IMAGE = 162_240
 # logic (ALU) pipe and instruction issue.  Its work per active window-step is
 # counted from the SASS of the library that runs (sass_loop_counts): the
 # innermost loop is one step of TWO windows per lane (64 per warp).
-HIDDEN_KERNEL = "_ZN3snn11k_hidden_gbILi3EEEvNS_9BatchArgsE"   # k_hidden_gb<3>
+HIDDEN_KERNEL = "_ZN3snn11k_hidden_gbILi3ELi20EEEvNS_9BatchArgsE"   # k_hidden_gb<3, 20>
 # SASS opcodes that issue to the ALU pipe (integer / logic / compare / select)
-ALU_OPS = ("LOP3", "LOP", "SHF", "ISETP", "IMNMX", "VIMNMX", "SEL", "FSEL", "FSETP", "FMNMX", "IADD3", "VIADD",
-           "LEA", "PRMT", "PLOP3", "BMSK", "FLO", "BREV", "SGXT")
+ALU_OPS = ("LOP3", "LOP", "SHF", "ISETP", "IMNMX", "VIMNMX", "VIMNMX3", "SEL", "FSEL", "FSETP", "FMNMX", "FMNMX3",
+           "IADD3", "VIADD", "LEA", "PRMT", "PLOP3", "BMSK", "FLO", "BREV", "SGXT")
 FP32_FLOP = {"FFMA2": 4, "FADD2": 2, "FMUL2": 2, "FFMA": 2, "FADD": 1, "FMUL": 1}
-SASS_FALLBACK = {"instructions": 259, "alu": 130, "fp32_flop": 242, "fp32_instr": 99, "windows_per_iter": 64,
-                 "ops": {"ISETP": 47, "LOP3": 42, "FADD2": 40, "FFMA2": 34, "SEL": 28, "FMUL": 24, "LDS": 18,
-                         "SHF": 10}}  # r02 v2 build, if cuobjdump is absent
+SASS_FALLBACK = {"instructions": 237, "alu": 112, "fp32_flop": 234, "fp32_instr": 95, "windows_per_iter": 64,
+                 "ops": {"LOP3": 40, "FADD2": 36, "FFMA2": 34, "ISETP": 24, "SEL": 24, "FMUL": 24, "LDS": 18,
+                         "VIMNMX3": 12, "SHF": 10}}  # r02 final build, if cuobjdump is absent
 LAUNCHES_PER_CHUNK = 6   # per sub-batch: k_prep, k_tile_scan, k_hidden_gb, k_hidden_fix, k_gsum, k_output
 PIPE_IMAGES = 0          # snn_set_pipeline sub-batch (library default: off)
 
