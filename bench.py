@@ -641,8 +641,10 @@ def kernel_table(stage_ms, call_ms, hidden_frac):
             e["frac"] = (n.get("issue_active_pct") or 0) / 100.0
             e["frac_basis"] = "issue slots busy (ncu smsp__issue_active); DRAM is dram_frac_of_hbm_peak"
         elif k == "k_output" and n:
-            e["frac"] = (n.get("fp64_pipe_pct") or 0) / 100.0
-            e["frac_basis"] = "FP64 pipe busy (ncu); each warp is one image's serial 10-neuron chain"
+            fp, iss = (n.get("fp64_pipe_pct") or 0) / 100.0, (n.get("issue_active_pct") or 0) / 100.0
+            e["frac"] = max(fp, iss)
+            e["bound"] = "issue (lane-distributed step, k_output_dist)" if iss >= fp else "fp64 pipe"
+            e["frac_basis"] = "the busier of the FP64 pipe and the issue slots (ncu); a warp is one image's serial chain"
         elif n:
             e["frac"] = (n.get("issue_active_pct") or 0) / 100.0
             e["frac_basis"] = "issue slots busy (ncu)"
