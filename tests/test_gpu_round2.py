@@ -316,3 +316,28 @@ def test_speculative_normad_bit_identical(sd, cfg, bank, workloads):
     assert res[4][2][0] == 0 and res[4][2][2] == n
     print(f"speculative scans redone: {res[4][2][3]} of {n - 1}")
     assert 0 <= res[4][2][3] < n
+
+
+def test_output_dist_bit_identical(sd, cfg, bank, workloads, wfix):
+    """The lane-distributed output layer (k_output_dist, batches >= 256) and
+    the replicated-trace one (snn_set_output_dist(0)): counts, ff, v_out and
+    the output raster of 300 config-3 images bit for bit."""
+    from paper_1711_03637_b200.engine import get_engine, make_consts
+    eng = get_engine()
+    c = make_consts(cfg, bank)
+    n = 300
+    imgs = torch.from_numpy(workloads["c3_images"][:n].reshape(n, -1).copy()).to(eng.device)
+    w = torch.from_numpy(wfix["w_fix"].copy()).to(eng.device)
+    res = []
+    for mode in (1, 0):
+        eng.lib.snn_set_output_dist(mode)
+        try:
+            o = eng.infer(c, imgs, w, trace=True)
+            o2 = eng.infer(c, imgs, w, raster=True)
+            eng.stream.synchronize()
+            res.append([o[k].cpu().numpy() for k in ("counts", "ff", "v_out")] + [o2["out_raster"].cpu().numpy()])
+        finally:
+            eng.lib.snn_set_output_dist(1)
+    assert res[0][0].sum() > 0
+    for a, b in zip(res[0], res[1]):
+        assert np.array_equal(a, b)
