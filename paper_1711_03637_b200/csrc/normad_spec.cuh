@@ -411,40 +411,88 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
                 if (i + 2 < n) gather(Pn, Gn, wt, kSpWorkers);
                 workers_sync();
                 SP_STAMP(32, 6)
-                // image i+3's lists: the workers other than warp 1 (which forms E)
-                if (warp != 1 && i + 3 < n) stage(i + 3, (int)((i + 3) % kSpBufs), wt - 32, kSpWorkers - 32);
-                if (spec && warp == 1) {
+                // image i+3's lists: the workers that do not form E (worker warps 5..)
+                if (wt >= 160 && i + 3 < n) stage(i + 3, (int)((i + 3) % kSpBufs), wt - 160, kSpWorkers - 160);
+                if (spec && wt < 160) {
                     // E(s, l): bound on |vn_exact - vn_spec| (header comment): d = G - G',
                     // its signed feed-forward response dA - dB, and the rounding of both
                     // runs bounded per output by constants (2^-40 x magnitudes of G, of
-                    // the A / B recursions and of every LIF operand)
-                    const int l = lane < kNO ? lane : kNO - 1;
+                    // the A / B recursions and of every LIF operand).  Every recurrence
+                    // is first-order linear, so it runs as a parallel scan: worker warp
+                    // k < 5 takes outputs 2k, 2k+1 (one per half-warp), lane j of a half
+                    // a block of K consecutive steps (an affine map carry -> lambda^len
+                    // carry + local), composed over the 16 lanes by shuffles.
+                    const int l = 2 * (wt >> 5) + (lane >> 4), j = lane & 15;
+                    const int K = (N + 15) >> 4, a0 = min(j * K, N), b0 = min(a0 + K, N);
                     const double ls = c.decay_slow, lf = c.decay_fast;
-                    const double K = 1.0 / (1.0 - ls) + 1.0 / (1.0 - lf);
+                    const double K2 = 1.0 / (1.0 - ls) + 1.0 / (1.0 - lf);
                     const double D = fabs(1.0 - po.beta * po.g);
-                    double gm = 0.0, dmx = 0.0;
-                    for (int s = 0; s < N; ++s) {
-                        const double x = Gx[s * kNO + l], y = Gs[s * kNO + l];
+                    // pass 1: local dA, dB (carry 0) and the magnitudes
+                    double dA = 0.0, dB = 0.0, pA = 1.0, pB = 1.0, gm = 0.0, dmx = 0.0;
+                    for (int t = a0; t < b0; ++t) {
+                        const double x = Gx[t * kNO + l], y = Gs[t * kNO + l], d = x - y;
+                        dA = __fma_rn(dA, ls, d);
+                        dB = __fma_rn(dB, lf, d);
+                        pA *= ls;
+                        pB *= lf;
                         gm = fmax(gm, fmax(fabs(x), fabs(y)));
-                        dmx = fmax(dmx, fabs(x - y));
+                        dmx = fmax(dmx, fabs(d));
                     }
+#pragma unroll
+                    for (int o = 1; o < 16; o <<= 1) {
+                        gm = fmax(gm, __shfl_xor_sync(kFull, gm, o));
+                        dmx = fmax(dmx, __shfl_xor_sync(kFull, dmx, o));
+                    }
+                    // forward composition of the blocks' maps (16-lane groups)
+                    double cA = dA, cB = dB, qA = pA, qB = pB;
+#pragma unroll
+                    for (int o = 1; o < 16; o <<= 1) {
+                        const double cA2 = __shfl_up_sync(kFull, cA, o, 16), qA2 = __shfl_up_sync(kFull, qA, o, 16);
+                        const double cB2 = __shfl_up_sync(kFull, cB, o, 16), qB2 = __shfl_up_sync(kFull, qB, o, 16);
+                        if (j >= o) {
+                            cA = __fma_rn(qA, cA2, cA);
+                            qA *= qA2;
+                            cB = __fma_rn(qB, cB2, cB);
+                            qB *= qB2;
+                        }
+                    }
+                    double inA = __shfl_up_sync(kFull, cA, 1, 16), inB = __shfl_up_sync(kFull, cB, 1, 16);
+                    if (j == 0) inA = inB = 0.0;
                     const double kR = 0x1p-40;
                     const double inh = fabs(c.inhibition) * kNO / (1.0 - ls);
-                    const double rA = kR * 2.0 * K * gm;                         // |A|, |B| roundings of both runs
+                    const double rA = kR * 2.0 * K2 * gm;
                     const double mag = fabs(po.el) + fabs(po.vt) + po.beta * po.g * (fabs(po.el) + fabs(po.vt)) +
-                                       po.beta * (K * gm + K * dmx + inh) + 1.0;  // every LIF operand
-                    // + the rounding of the computed dA - dB itself (it may cancel; its
-                    // terms' errors do not): 2^-40 x 2 K^2 max |d|
-                    const double cst = po.beta * (rA + kR * 2.0 * K * K * dmx) + kR * mag;
-                    const double infv = __longlong_as_double(0x7ff0000000000000LL);
-                    double dA = 0.0, dB = 0.0, E = 0.0;
-#pragma unroll 4
-                    for (int s = 0; s < N; ++s) {
-                        const double d = Gx[s * kNO + l] - Gs[s * kNO + l];
+                                       po.beta * (K2 * gm + K2 * dmx + inh) + 1.0;
+                    const double cst = po.beta * (rA + kR * 2.0 * K2 * K2 * dmx) + kR * mag;
+                    // pass 2: dA, dB from their carries; local E (carry 0)
+                    dA = inA;
+                    dB = inB;
+                    double E = 0.0, pE = 1.0;
+                    for (int t = a0; t < b0; ++t) {
+                        const double d = Gx[t * kNO + l] - Gs[t * kNO + l];
                         dA = __fma_rn(dA, ls, d);
                         dB = __fma_rn(dB, lf, d);
                         E = __fma_rn(E, D, __fma_rn(po.beta, fabs(dA - dB) * (1.0 + 0x1p-40), cst));
-                        if (lane < kNO) Eb[s * kNO + lane] = D < 1.0 ? E * (1.0 + 0x1p-20) : infv;
+                        pE *= D;
+                        Eb[t * kNO + l] = E;
+                    }
+                    double cE = E, qE = pE;
+#pragma unroll
+                    for (int o = 1; o < 16; o <<= 1) {
+                        const double cE2 = __shfl_up_sync(kFull, cE, o, 16), qE2 = __shfl_up_sync(kFull, qE, o, 16);
+                        if (j >= o) {
+                            cE = __fma_rn(qE, cE2, cE);
+                            qE *= qE2;
+                        }
+                    }
+                    double inE = __shfl_up_sync(kFull, cE, 1, 16);
+                    if (j == 0) inE = 0.0;
+                    // pass 3: E with its carry (all terms >= 0; rounded up by 2^-20)
+                    const double infv = __longlong_as_double(0x7ff0000000000000LL);
+                    double pw = 1.0;
+                    for (int t = a0; t < b0; ++t) {
+                        pw *= D;
+                        Eb[t * kNO + l] = D < 1.0 ? __fma_rn(pw, inE, Eb[t * kNO + l]) * (1.0 + 0x1p-20) : infv;
                     }
                 }
             }
