@@ -275,8 +275,28 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
     const int rows = cl_rows(r);
     if (T.status[0] != 0) return;  // an earlier chunk failed (uniform over the cluster)
     double *undo = SW.undo + (size_t)r * kClRows * kNO;
-    for (int t = tid; t < rows * kNO; t += kClThreads)
+#ifdef SNN_W_TMA
+    // the W shard by TMA bulk copies: window w = r + 8 j owns 12 consecutive
+    // rows (960 B) of W, so one cp.async.bulk per window into the shard's
+    // rows 12 j .. 12 j + 11, all on one mbarrier.  Built only with
+    // -DSNN_W_TMA: the 82 KB load is once per chunk of ~320 images either
+    // way, and this variant moved the serial scan's register allocation
+    // (19.27 vs 19.00 us per image)
+    __shared__ __align__(8) uint64_t s_wbar;
+    if (tid == 0) {
+        mbar_init(&s_wbar, 1);
+        fence_mbar_init();
+        const int nw = rows / kNF;
+        mbar_expect_tx(&s_wbar, (uint32_t)(rows * kNO * 8));
+        for (int j = 0; j < nw; ++j)
+            bulk_g2s(Wsh + (size_t)j * kNF * kNO, T.w + (size_t)((j * kCl + r) * kNF) * kNO, kNF * kNO * 8, &s_wbar);
+    }
+    __syncthreads();
+    mbar_wait(&s_wbar, 0);
+#else
+    for (int t = tid; t < rows * kNO; t += kClThreads)  // once per chunk (L2-coherent loads)
         Wsh[t] = __ldcg(T.w + (size_t)cl_id(r, t / kNO) * kNO + t % kNO);
+#endif
     if (tid < kCl) flags[tid] = 0;
     double *PQ_lead = cluster.map_shared_rank(PQ, 0) + (size_t)r * N * kNO;  // this CTA's partials there
     int *flags_lead = cluster.map_shared_rank(flags, 0);
