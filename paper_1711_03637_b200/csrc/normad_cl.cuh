@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kShThreads) k_shard(const TrainArgs T, const S
     }
     __syncthreads();
     uint16_t *sact = S.sact + (size_t)i * kNH, *sidx = S.sidx + (size_t)i * kNH;
+#ifdef SNN_SHARD_STABLE
     for (int a0 = 0; a0 < n_act; a0 += kShThreads) {
         const int a = a0 + tid;
         const int r = a < n_act ? cl_shard(act_k[a]) : -1;
@@ -161,6 +162,33 @@ __global__ void __launch_bounds__(kShThreads) k_shard(const TrainArgs T, const S
             for (int w = 0; w < kWarps; ++w) s_run[tid] += s_wc[w][tid];
         __syncthreads();
     }
+#else
+    // within a shard, neurons by descending spike count (buckets of 0..31+
+    // spikes): the cluster kernel's dW gives thread t row t / 5 in rounds of
+    // its 512 threads, so the heaviest rows share the first round instead of
+    // lengthening every round.  Each row's update is independent of the
+    // order (same weights bit for bit); positions inside a bucket come from
+    // shared-memory atomics.
+    __shared__ int s_bk[kCl][32];
+    for (int k = tid; k < kCl * 32; k += kShThreads) (&s_bk[0][0])[k] = 0;
+    __syncthreads();
+    for (int a = tid; a < n_act; a += kShThreads)
+        atomicAdd(&s_bk[cl_shard(act_k[a])][31 - min(aoff[a + 1] - aoff[a], 31)], 1);
+    __syncthreads();
+    if (warp < kCl) {  // warp r: exclusive prefix of shard r's 32 buckets -> cursors
+        int tot;
+        const int ex = warp_excl_scan_int(s_bk[warp][lane], &tot);
+        s_bk[warp][lane] = s_abase[warp] + ex;
+    }
+    __syncthreads();
+    for (int a = tid; a < n_act; a += kShThreads) {
+        const int r = cl_shard(act_k[a]);
+        const int pos = atomicAdd(&s_bk[r][31 - min(aoff[a + 1] - aoff[a], 31)], 1);
+        sact[pos] = (uint16_t)cl_row(act_k[a]);
+        sidx[pos] = (uint16_t)a;
+    }
+    __syncthreads();
+#endif
     // per-shard spike-block offsets: warp r walks shard r's neurons in order
     int32_t *saoff = S.saoff + (size_t)i * (kNH + kCl);
     if (warp < kCl) {
