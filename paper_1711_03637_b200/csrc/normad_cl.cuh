@@ -118,8 +118,11 @@ __global__ void __launch_bounds__(kShThreads) k_shard(const TrainArgs T, const S
     const uint16_t *nsp = W.nsp + (size_t)i * W.evcap;
     const int32_t *soff = W.step_off + (size_t)i * (N + 1);
     const uint16_t *sk = W.step_k + (size_t)i * W.evcap;
-    __shared__ int s_cnt[kCl], s_run[kCl], s_abase[kCl + 1], s_nbase[kCl + 1], s_ebase[kCl + 1];
+    __shared__ int s_cnt[kCl], s_abase[kCl + 1], s_nbase[kCl + 1], s_ebase[kCl + 1];
+#ifdef SNN_SHARD_STABLE
+    __shared__ int s_run[kCl];
     __shared__ int s_wc[kWarps][kCl];
+#endif
     extern __shared__ int s_len[];  // [N][kCl] step-list counts, then offsets
     for (int s = tid; s < N; s += kShThreads) {
         const double nv = W.norm[(size_t)i * N + s];
@@ -127,7 +130,9 @@ __global__ void __launch_bounds__(kShThreads) k_shard(const TrainArgs T, const S
     }
     if (tid < kCl) {
         s_cnt[tid] = 0;
+#ifdef SNN_SHARD_STABLE
         s_run[tid] = 0;
+#endif
     }
     __syncthreads();
     // ---- active neurons: counts and spike totals per shard, then a stable partition
