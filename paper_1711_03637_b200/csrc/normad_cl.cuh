@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kShThreads) k_shard(const TrainArgs T, const S
     const int N = T.c.n_steps;
     const TrainWS &W = T.ws;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int kWarps = kShThreads / 32;
+    [[maybe_unused]] constexpr int kWarps = kShThreads / 32;
     const int n_act = W.n_act[i];
     const uint16_t *act_k = W.act_k + (size_t)i * kNH;
     const int32_t *aoff = W.act_off + (size_t)i * (kNH + 1);
