@@ -887,9 +887,15 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t x) {
     return x;
 }
 
+// A step list's row stride: CAP + 8 ids (16 bytes) shifts consecutive rows by
+// four banks, so the 8 list writers (one per step) and the 6 readers of a sums
+// round hit distinct banks; rows stay 16-byte aligned for the 8-id loads.
+template <int CAP>
+constexpr int ids_stride() { return CAP + 8; }
+
 template <int CAP>
 struct GsumSmem {
-    uint16_t ids[kChunk * CAP];       // the chunk's step lists
+    alignas(16) uint16_t ids[kChunk * ids_stride<CAP>()];  // the chunk's step lists
     uint16_t pos[kMaxTiles * kTile];  // window position of each (tile, lane)
     uint64_t pl[2][kTile];            // the current tile's two mask planes, per window
 };
@@ -949,7 +955,7 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
         if (g >= 2) inc += y;
         const unsigned tot = __shfl_sync(kFull, inc, lane | 3);
         unsigned k = runl + inc - cnt;
-        uint16_t *dst = S.ids + jl * kStepCap;
+        uint16_t *dst = S.ids + jl * ids_stride<CAP>();
         const uint16_t *tp = PP + t * kTile + g;
         // one loop over all of this lane's spikes: 12-bit fields of windows 0..4 and 5..7
         uint64_t w0 = (uint64_t)m[0] | ((uint64_t)m[1] << 12) | ((uint64_t)m[2] << 24) | ((uint64_t)m[3] << 36) |
@@ -977,14 +983,17 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
         const int j = j0 + lane / 5, p = lane % 5;
         const unsigned cnt = __shfl_sync(kFull, runl, (j & 7) * 4);
         if (lane < 30 && j < ns && cnt <= kStepCap) {
-            const uint16_t *lst = S.ids + j * kStepCap;
+            const uint16_t *lst = S.ids + j * ids_stride<CAP>();
             const double2 *W2 = reinterpret_cast<const double2 *>(W) + p;
             double g0 = 0.0, g1 = 0.0, a0 = 0.0, a1 = 0.0;
             unsigned e = 0;
             for (; e + 8 <= cnt; e += 8) {
+                const uint4 q = *reinterpret_cast<const uint4 *>(lst + e);  // 8 ids in one load
+                const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
                 double2 v[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = __ldg(W2 + (size_t)lst[e + u] * (kNO / 2));
+                for (int u = 0; u < 8; ++u)
+                    v[u] = __ldg(W2 + (size_t)((qw[u >> 1] >> (16 * (u & 1))) & 0xFFFFu) * (kNO / 2));
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     g0 = __dadd_rn(g0, v[u].x);
