@@ -863,7 +863,10 @@ __device__ __forceinline__ bool outd_step(OutD &X, const snn_consts_t &c, double
 //   sums   lane (j, p) walks step j's list for outputs 2p, 2p+1 (16-byte W
 //          loads, 8 in flight).  A step with more than kStepCap spikes is
 //          summed afterwards tile by tile in ascending neuron id.
-constexpr int kStepCap = 256;
+#ifndef SNN_GSUM_CAP
+#define SNN_GSUM_CAP 192
+#endif
+constexpr int kStepCap = SNN_GSUM_CAP;
 constexpr int kGWarps = 4;
 
 __device__ __forceinline__ uint32_t byte_popc(uint32_t x) {  // popcount of each byte
@@ -892,6 +895,7 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t x) {
 // round hit distinct banks; rows stay 16-byte aligned for the 8-id loads.
 template <int CAP>
 constexpr int ids_stride() { return CAP + 8; }
+static_assert(kNO % 2 == 0 && kNH * (kNO / 2) <= 0xFFFF, "list entries: W row offsets in double2 units fit 16 bits");
 
 template <int CAP>
 struct GsumSmem {
@@ -957,27 +961,31 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
         unsigned k = runl + inc - cnt;
         uint16_t *dst = S.ids + jl * ids_stride<CAP>();
         const uint16_t *tp = PP + t * kTile + g;
-        // one loop over all of this lane's spikes: 12-bit fields of windows 0..4 and 5..7
-        uint64_t w0 = (uint64_t)m[0] | ((uint64_t)m[1] << 12) | ((uint64_t)m[2] << 24) | ((uint64_t)m[3] << 36) |
-                      ((uint64_t)m[4] << 48);
-        uint64_t w1 = (uint64_t)m[5] | ((uint64_t)m[6] << 12) | ((uint64_t)m[7] << 24);
-        while (w0 | w1) {
-            const bool lo = w0 != 0ull;
-            const uint64_t w = lo ? w0 : w1;
-            const int b = __ffsll((long long)w) - 1 + (lo ? 0 : 60);
-            if (lo) w0 &= w0 - 1ull;
-            else w1 &= w1 - 1ull;
-            const int i = (b * 43) >> 9;  // b / 12 for b < 96
-            if (k < (unsigned)kStepCap) dst[k] = (uint16_t)((int)tp[4 * i] * kNF + (b - 12 * i));
-            ++k;
+        // window pairs (2q, 2q+1) as 24-bit words, spikes taken highest bit
+        // first (window 2q+1 before 2q, features descending): a fixed order
+        // per image, and one FLO + one clear per spike.
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t w = m[2 * q] | (m[2 * q + 1] << 12);
+            if (w) {
+                // list entries are W row offsets in double2 units: neuron id * kNO / 2
+                constexpr int kR = kNO / 2;
+                const int r0 = (int)tp[8 * q] * (kNF * kR), r1 = (int)tp[8 * q + 4] * (kNF * kR) - 12 * kR;
+                do {
+                    const int b = 31 - __clz(w);
+                    w &= ~(1u << b);
+                    if (k < (unsigned)kStepCap) dst[k] = (uint16_t)((b >= 12 ? r1 : r0) + kR * b);
+                    ++k;
+                } while (w);
+            }
         }
         runl += tot;
     }
     __syncwarp();
     // steps whose list overflowed kStepCap (bit j), warp-uniform
     const unsigned ovf = __ballot_sync(kFull, g == 0 && runl > (uint32_t)kStepCap) ;
-    // ---- sums: lane (j, p) -> G[j][2p], G[j][2p+1]; rounds of 6 steps
     double *Gi = G + ((size_t)img * N + s0) * kNO;
+    // ---- sums: lane (j, p) -> G[j][2p], G[j][2p+1]; rounds of 6 steps
 #pragma unroll 1
     for (int j0 = 0; j0 < ns; j0 += 6) {
         const int j = j0 + lane / 5, p = lane % 5;
@@ -992,8 +1000,7 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
                 const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
                 double2 v[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    v[u] = __ldg(W2 + (size_t)((qw[u >> 1] >> (16 * (u & 1))) & 0xFFFFu) * (kNO / 2));
+                for (int u = 0; u < 8; ++u) v[u] = __ldg(W2 + ((qw[u >> 1] >> (16 * (u & 1))) & 0xFFFFu));
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     g0 = __dadd_rn(g0, v[u].x);
@@ -1005,7 +1012,7 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
                 }
             }
             for (; e < cnt; ++e) {
-                const double2 v = __ldg(W2 + (size_t)lst[e] * (kNO / 2));
+                const double2 v = __ldg(W2 + lst[e]);
                 g0 = __dadd_rn(g0, v.x);
                 g1 = __dadd_rn(g1, v.y);
                 if (ABS) {
@@ -1052,8 +1059,11 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
     }
 }
 
+#ifndef SNN_GSUM_MINB
+#define SNN_GSUM_MINB 9
+#endif
 template <bool ABS>
-__global__ void __launch_bounds__(kGWarps * 32) k_gsum(const BatchArgs A, double *G, double *Gabs) {
+__global__ void __launch_bounds__(kGWarps * 32, SNN_GSUM_MINB) k_gsum(const BatchArgs A, double *G, double *Gabs) {
     __shared__ __align__(16) GsumSmem<kStepCap> smem[kGWarps];
     const int warp = threadIdx.x >> 5;
     const int nch = n_chunks(A.c.n_steps);
