@@ -901,7 +901,6 @@ template <int CAP>
 struct GsumSmem {
     alignas(16) uint16_t ids[kChunk * ids_stride<CAP>()];  // the chunk's step lists
     uint16_t pos[kMaxTiles * kTile];  // window position of each (tile, lane)
-    uint64_t pl[2][kTile];            // the current tile's two mask planes, per window
 };
 
 // One (image, chunk) task of one warp: lists, then sums, into G's chunk rows.
@@ -929,28 +928,47 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
         n0 = __ldcs(reinterpret_cast<const unsigned long long *>(R));
         n1 = __ldcs(reinterpret_cast<const unsigned long long *>(R + kRastTC / 2));
     }
-    const uint8_t *b0 = reinterpret_cast<const uint8_t *>(S.pl[0]) + jl, *b1 = reinterpret_cast<const uint8_t *>(S.pl[1]) + jl;
+    // 8x8 byte transpose among lanes g, g+4, .., g+28 (three butterfly
+    // stages, shuffles xor 16 / 8 / 4): lane (jl, g) then holds byte jl (step
+    // jl) of the planes of windows g + 4i in byte i.  Per-lane byte selectors:
+    const int ti = lane >> 2;
+    const uint32_t s2s = (ti & 2) ? 0x5410u : 0x7632u, s2l = (ti & 2) ? 0x3254u : 0x5410u,
+                   s2h = (ti & 2) ? 0x3276u : 0x7610u;
+    const uint32_t s3s = (ti & 1) ? 0x6420u : 0x7531u, s3l = (ti & 1) ? 0x3514u : 0x5240u,
+                   s3h = (ti & 1) ? 0x3716u : 0x7260u;
+    auto transpose = [&](uint64_t v, uint32_t &lo, uint32_t &hi) {
+        lo = (uint32_t)v;
+        hi = (uint32_t)(v >> 32);
+        const uint32_t r1 = __shfl_xor_sync(kFull, (ti & 4) ? lo : hi, 16);
+        if (ti & 4) lo = r1;
+        else hi = r1;
+        const uint32_t r2 = __shfl_xor_sync(kFull, __byte_perm(lo, hi, s2s), 8);
+        lo = __byte_perm(lo, r2, s2l);
+        hi = __byte_perm(hi, r2, s2h);
+        const uint32_t r3 = __shfl_xor_sync(kFull, __byte_perm(lo, hi, s3s), 4);
+        lo = __byte_perm(lo, r3, s3l);
+        hi = __byte_perm(hi, r3, s3h);
+    };
     for (int t = 0; t < nt; ++t) {
-        __syncwarp();
         if (PP[t * kTile + lane] == 0xFFFF) n0 = n1 = 0ull;  // raster bytes exist only for windows
-        S.pl[0][lane] = n0;
-        S.pl[1][lane] = n1;
         const bool any = __any_sync(kFull, (n0 | n1) != 0ull);
+        uint32_t p0l, p0h, p1l, p1h;
+        if (any) {
+            transpose(n0, p0l, p0h);
+            transpose(n1, p1l, p1h);
+        }
         if (t + 1 < nt) {
             const uint8_t *nxt = R + (size_t)(t + 1) * kRastTC;
             n0 = __ldcs(reinterpret_cast<const unsigned long long *>(nxt));
             n1 = __ldcs(reinterpret_cast<const unsigned long long *>(nxt + kRastTC / 2));
         }
         if (!any) continue;  // warp-uniform: no spike in this tile-chunk
-        __syncwarp();
-        unsigned m[8];
-        unsigned cnt = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int w = i * 4 + g;  // interleaved: spatially clustered spikes spread over the 4 lanes
-            m[i] = (unsigned)b0[w * 8] | ((unsigned)b1[w * 8] << kHalf);
-            cnt += __popc(m[i]);
-        }
+        // word q: windows g + 8q (bytes 0, 2: features 0-5, 6-11) and g + 8q + 4
+        // (bytes 1, 3); interleaved windows spread spatially clustered spikes
+        // over the 4 lanes of a step
+        const uint32_t wq[4] = {__byte_perm(p0l, p1l, 0x5410u), __byte_perm(p0l, p1l, 0x7632u),
+                                __byte_perm(p0h, p1h, 0x5410u), __byte_perm(p0h, p1h, 0x7632u)};
+        const unsigned cnt = __popc(wq[0]) + __popc(wq[1]) + __popc(wq[2]) + __popc(wq[3]);
         // prefix over the 4 window groups of step jl
         unsigned inc = cnt;
         unsigned y = __shfl_up_sync(kFull, inc, 1);
@@ -958,24 +976,31 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
         y = __shfl_up_sync(kFull, inc, 2);
         if (g >= 2) inc += y;
         const unsigned tot = __shfl_sync(kFull, inc, lane | 3);
-        unsigned k = runl + inc - cnt;
         uint16_t *dst = S.ids + jl * ids_stride<CAP>();
+        // shared-window byte addresses of this lane's next list slot and of the cap slot
+        const uint32_t scap = (uint32_t)__cvta_generic_to_shared(dst + kStepCap);
+        uint32_t sk = (uint32_t)__cvta_generic_to_shared(dst) + 2u * (runl + inc - cnt);
         const uint16_t *tp = PP + t * kTile + g;
-        // window pairs (2q, 2q+1) as 24-bit words, spikes taken highest bit
-        // first (window 2q+1 before 2q, features descending): a fixed order
-        // per image, and one FLO + one clear per spike.
+        // spikes taken highest bit first (a fixed order per image), one FLO
+        // and one clear per spike; bit b: window byte (b >> 3) & 1, feature
+        // (b & 7) + 6 (b >> 4)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            uint32_t w = m[2 * q] | (m[2 * q + 1] << 12);
+            uint32_t w = wq[q];
             if (w) {
                 // list entries are W row offsets in double2 units: neuron id * kNO / 2
                 constexpr int kR = kNO / 2;
-                const int r0 = (int)tp[8 * q] * (kNF * kR), r1 = (int)tp[8 * q + 4] * (kNF * kR) - 12 * kR;
+                // b = 16 plane + 8 window + feature-in-plane t:
+                // id * kR = r_window + kR t + kHalf kR plane = kR b + r'_window - (16 - kHalf) kR plane
+                const int r0 = (int)tp[8 * q] * (kNF * kR), r1 = (int)tp[8 * q + 4] * (kNF * kR) - 8 * kR;
                 do {
-                    const int b = 31 - __clz(w);
+                    int b;
+                    asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(w));  // highest set bit
                     w &= ~(1u << b);
-                    if (k < (unsigned)kStepCap) dst[k] = (uint16_t)((b >= 12 ? r1 : r0) + kR * b);
-                    ++k;
+                    const int e = kR * b + ((b & 8) ? r1 : r0) - (16 - kHalf) * kR * (b >> 4);
+                    // past the cap: the row's padding slot (never read)
+                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(min(sk, scap)), "h"((unsigned short)e));
+                    sk += 2;
                 } while (w);
             }
         }
@@ -1060,7 +1085,7 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
 }
 
 #ifndef SNN_GSUM_MINB
-#define SNN_GSUM_MINB 9
+#define SNN_GSUM_MINB 10
 #endif
 template <bool ABS>
 __global__ void __launch_bounds__(kGWarps * 32, SNN_GSUM_MINB) k_gsum(const BatchArgs A, double *G, double *Gabs) {
