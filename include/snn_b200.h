@@ -167,12 +167,13 @@ void snn_set_pipeline(int64_t images_per_subbatch, int hidden_ctas_per_sm);
 void snn_set_hidden_resident(int enable);
 
 /* snn_train runs its sequential NormAD chain on a cluster of 8 CTAs that
- * keeps W in distributed shared memory.  enable = 1 (default) or 3: the
- * cluster kernel with the G partials pushed to the leader when its shared
- * memory fits, else pulled (2 forces pulling), else one CTA (0 forces it);
- * 4: the kernel whose output scan of image i+1 runs speculatively during
- * image i's update and is proven or redone (normad_spec.cuh; experimental,
- * slower so far).  All give the same weights (1-4 bit for bit). */
+ * keeps W in distributed shared memory.  enable = 4 (default): the kernel
+ * whose output scan of image i+1 runs speculatively during image i's update
+ * and is proven or redone (normad_spec.cuh; d_status[3] counts the redone
+ * scans), when its shared memory fits, else as 1; 1 or 3: the cluster kernel
+ * with the G partials pushed to the leader when its shared memory fits, else
+ * pulled (2 forces pulling), else one CTA (0 forces it).  All give the same
+ * weights (1-4 bit for bit). */
 void snn_set_normad_cluster(int enable);
 
 /* The output layer of batches of >= 256 images uses the lane-distributed

@@ -22,6 +22,7 @@ SNN_ECUDA = 1002
 
 MAX_TILES = 22
 TILE = 32
+NORMAD_DEFAULT = 4   # snn_set_normad_cluster default: the speculative-scan kernel
 RASTER_CHUNK = 8
 
 

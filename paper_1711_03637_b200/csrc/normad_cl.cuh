@@ -38,6 +38,11 @@
 
 namespace snn {
 
+#ifdef SNN_SCAN_STAMPS
+// experiment builds only: clock64() at every step of image SNN_SCAN_STAMPS's output scan
+__device__ long long g_scan_stamps[256];
+#endif
+
 namespace cg = cooperative_groups;
 
 constexpr int kCl = 8;                          // CTAs per cluster = W shards
@@ -477,10 +482,19 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 1)
                 X.o.Bf = __dadd_rn(__dmul_rn(0.0, c.decay_fast), gp[0]);
                 X.D0 = __dadd_rn(__dsub_rn(X.o.Af, X.o.Bf), __dmul_rn(c.inhibition, __dsub_rn(0.0, 0.0)));
                 const int ns = (skip & 1) ? 0 : N;
+#ifdef SNN_SCAN_STAMPS
+                long long *stp = (T.first + i == SNN_SCAN_STAMPS && cluster.block_rank() == 0) ? g_scan_stamps : nullptr;
+#endif
                 for (int s = 0; s < ns; ++s) {
+#ifdef SNN_SCAN_STAMPS
+                    if (stp && lane == 0) stp[s] = clock64();
+#endif
                     outd_step(X, c, gp[(s + 1 < N ? s + 1 : s) * kNO], s, l);
                     if (lane == 0) om[s] = (uint16_t)X.o.prev;
                 }
+#ifdef SNN_SCAN_STAMPS
+                if (stp && lane == 0) stp[ns] = clock64();
+#endif
                 if (lane < kNO) T.counts[(size_t)i * kNO + lane] = X.o.cnt;
 #ifdef SNN_NORMAD_PROFILE
                 if (clk && lane == 0) clk[12] = clock64();

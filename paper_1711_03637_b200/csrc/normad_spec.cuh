@@ -122,26 +122,56 @@ __device__ __forceinline__ bool outd_step_m(OutD &X, const snn_consts_t &c, doub
 #endif
 template <bool MARGIN>
 __device__ SNN_SCAN_INLINE int spec_scan(const snn_consts_t &c, const double *G, uint16_t *om, int N,
-                                         double *M) {
+                                         double *M, long long *stp = nullptr) {
     const int lane = threadIdx.x & 31;
     const int l = lane < kNO ? lane : kNO - 1;
+    // Register copies of the constants a step reads, passed through a shuffle
+    // so ptxas cannot re-read them from the constant bank: under this
+    // kernel's uniform-register pressure it otherwise reloads them (LDCU)
+    // inside the loop, on the step's dependency chain (358 against 233
+    // cycles per step, scripts/scan_stamps.py).
+    snn_consts_t k;
+    k.lif_out = c.lif_out;
+    k.decay_slow = c.decay_slow;
+    k.decay_fast = c.decay_fast;
+    k.inhibition = c.inhibition;
+    {
+        double *v[8] = {&k.lif_out.g, &k.lif_out.el, &k.lif_out.vt, &k.lif_out.beta,
+                        &k.lif_out.refr, &k.decay_slow, &k.decay_fast, &k.inhibition};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+#ifndef SNN_SPEC_NOLAUNDER
+            *v[q] = __shfl_sync(kFull, *v[q], 0);  // opaque to ptxas
+#endif
+        }
+    }
     OutD X;
-    out_init(X.o, c);
+    out_init(X.o, k);
     const double *gp = G + l;
     X.o.Af = __dadd_rn(__dmul_rn(0.0, c.decay_slow), gp[0]);
     X.o.Bf = __dadd_rn(__dmul_rn(0.0, c.decay_fast), gp[0]);
     X.D0 = __dadd_rn(__dsub_rn(X.o.Af, X.o.Bf), __dmul_rn(c.inhibition, __dsub_rn(0.0, 0.0)));
     for (int s = 0; s < N; ++s) {
+#ifdef SNN_SCAN_STAMPS
+        if (stp && lane == 0) stp[s] = clock64();
+#endif
         const double Gn = gp[(s + 1 < N ? s + 1 : s) * kNO];
+        // unconditional stores (lanes >= kNO repeat lane kNO - 1's values, and
+        // om[s] is the same ballot in every lane): a branch around them would
+        // keep ptxas from overlapping the next step's feed-forward sums with
+        // this step's membrane chain
         if (MARGIN) {
             double m;
-            outd_step_m(X, c, Gn, s, l, m);
-            if (lane < kNO) M[s * kNO + lane] = m;
+            outd_step_m(X, k, Gn, s, l, m);
+            M[s * kNO + l] = m;
         } else {
-            outd_step(X, c, Gn, s, l);
+            outd_step(X, k, Gn, s, l);
         }
-        if (lane == 0) om[s] = (uint16_t)X.o.prev;
+        om[s] = (uint16_t)X.o.prev;
     }
+#ifdef SNN_SCAN_STAMPS
+    if (stp && lane == 0) stp[N] = clock64();
+#endif
     return X.o.cnt;
 }
 
@@ -334,7 +364,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
             // (and warp 0 elsewhere) leave the scan warp's partition idle
             cl_arrive();
 #ifndef SNN_SPEC_NOSPEC
+#ifdef SNN_SCAN_STAMPS
+            if (r == 0 && spec && warp == 0)
+                cnt = spec_scan<true>(c, Gs, OMs, N, Mg, T.first + i + 1 == SNN_SCAN_STAMPS ? g_scan_stamps : nullptr);
+#else
             if (r == 0 && spec && warp == 0) cnt = spec_scan<true>(c, Gs, OMs, N, Mg);
+#endif
 #endif
             SP_STAMP(0, 1)
             cl_wait();

@@ -199,7 +199,7 @@ struct Knobs {
     int hid_gb_small = 0;              // ... also below kGbMinImages (snn_set_hidden_resident(5), tests)
     int out_dist = 1;                  // k_output_dist for large batches (snn_set_output_dist)
     int hid_fz = SNN_HID_FZ;           // -DSNN_HID_FZ=0: never the frozen-mask variant (A/B builds)
-    int normad_cluster = 1;            // snn_set_normad_cluster
+    int normad_cluster = 4;            // snn_set_normad_cluster (4: speculative scan)
     long long *phase_clk = nullptr;    // snn_normad_phase_clocks
     int normad_skip = 0;               // snn_normad_skip (profiling only)
     int64_t pipe_images = 0;           // snn_set_pipeline
@@ -450,6 +450,12 @@ extern "C" void snn_profile_stage_events(void *const *events, int n_events) {
 
 extern "C" const char *snn_last_error(void) { return g_err; }
 
+#ifdef SNN_SCAN_STAMPS
+extern "C" int snn_debug_scan_stamps(long long *out, int n) {
+    return cudaMemcpyFromSymbol(out, snn::g_scan_stamps, sizeof(long long) * (size_t)std::min(n, 256)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
 extern "C" int snn_input_table(const snn_consts_t *c, double *d_ctab, uint8_t *d_spk, void *stream) {
     int rc = validate(c);
     if (rc) return rc;
@@ -588,12 +594,13 @@ extern "C" int snn_train(const snn_consts_t *c, const uint8_t *d_images, const u
     if (c->n_steps > 65535) return set_error(SNN_EINVAL, "training supports n_steps <= 65535");
     // the W-resident cluster kernel when its shared memory fits, else the one-CTA kernel
     const Knobs &K = knobs();
-    // mode 1 (default) / 3: the cluster kernel (partials pushed), 2: pulled;
-    // 4: the speculative-scan cluster kernel (normad_spec.cuh, experimental:
-    // bit-identical weights, slower so far -- DESIGN.md 4.1); 0: one CTA.
+    // mode 4 (default): the speculative-scan cluster kernel (normad_spec.cuh,
+    // DESIGN.md 4.1) when its shared memory fits, else mode 1; 1 / 3: the
+    // cluster kernel (partials pushed), 2: pulled; 0: one CTA.  1-4 give the
+    // same weights bit for bit.
     const size_t sp_smem = normad_spec_smem_bytes(c->n_steps);
     const bool use_spec = K.normad_cluster == 4 && sp_smem <= 227 * 1024;
-    const bool cl_push = (K.normad_cluster == 1 || K.normad_cluster == 3) &&
+    const bool cl_push = (K.normad_cluster == 1 || K.normad_cluster == 3 || K.normad_cluster == 4) &&
                          normad_cl_smem_bytes(c->n_steps, true) <= 227 * 1024;
     // long trials: sigma/R reuse the G array, so the cluster kernel fits up to N ~ 1,300
     const bool cl_alias = !cl_push && normad_cl_smem_bytes(c->n_steps, false) > 227 * 1024;

@@ -268,6 +268,9 @@ class Engine:
         Returns (counts int32 [n,10] device, status int32 [4] device)."""
         torch = _torch()
         n = int(images.shape[0])
+        assert images.dtype == torch.uint8 and images.is_contiguous() and tuple(images.shape[1:]) == (N_INPUTS,)
+        assert labels.dtype == torch.uint8 and labels.is_contiguous() and tuple(labels.shape) == (n,)
+        assert w.dtype == torch.float64 and w.is_contiguous() and tuple(w.shape) == (N_HIDDEN, N_OUTPUTS)
         ctab, _ = self.table(c)
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream):

@@ -34,4 +34,4 @@ for mode in (1, 0):
         ts.append(e0.elapsed_time(e1))
     print(f"dt=0.1ms training cluster={mode}: {statistics.median(ts[1:]) / len(order) * 1e3:.1f} us/image "
           f"({len(order) / statistics.median(ts[1:]) * 1e3:.0f} img/s)")
-eng.lib.snn_set_normad_cluster(1)
+eng.lib.snn_set_normad_cluster(4)

@@ -12,7 +12,7 @@ d = np.load(os.path.join(ROOT, "data", "workloads.npz"))
 eng = get_engine()
 c = make_consts(sd.NetworkConfig(), sd.default_filter_bank(), sd.LearnConfig())
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
-order = d["c2_order"][:n]
+order = np.resize(d["c2_order"], n)  # the 1,000-image c2 set, repeated past its end
 imgs = torch.from_numpy(d["c2_images"][order].reshape(n, -1).copy()).cuda()
 labs = torch.from_numpy(d["c2_labels"][order].astype(np.uint8)).cuda()
 res = {}
@@ -30,7 +30,7 @@ for mode in (3, 4):
     st = status.cpu().numpy()
     res[mode] = (dw.cpu().numpy(), cnt.cpu().numpy())
     print(f"mode {mode}: {statistics.median(ts[2:]) * 1e3 / n:.2f} us/image  status {st}", flush=True)
-eng.lib.snn_set_normad_cluster(1)
+eng.lib.snn_set_normad_cluster(4)
 w3, w1 = res[3][0], res[4][0]
 print("weights bitwise equal:", bool(np.array_equal(w3, w1)), " max|dw|", float(np.abs(w3 - w1).max()))
 print("counts equal:", bool(np.array_equal(res[3][1], res[4][1])))

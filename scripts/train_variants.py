@@ -24,4 +24,4 @@ for mode in (1, 2, 0, 1, 2):
     w = dw.cpu().numpy()
     ref = w if ref is None else ref
     print(f"mode {mode}: {min(ts):.2f} ms  {1000 / min(ts) * 1e3:.0f} img/s  max|dW vs mode1| {np.abs(w - ref).max():.3e}", flush=True)
-eng.lib.snn_set_normad_cluster(1)
+eng.lib.snn_set_normad_cluster(4)

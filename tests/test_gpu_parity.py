@@ -16,6 +16,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
+from paper_1711_03637_b200 import _native  # noqa: E402
 if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
@@ -417,12 +418,14 @@ def test_hidden_kernel_variants_identical(sd, cfg, bank, workloads, wfix):
     order = workloads["c2_order"][:40]
     ims, labs = workloads["c2_images"][order], workloads["c2_labels"][order]
     res = []
-    for cl in (1, 2, 0):  # cluster (partials pushed / pulled) and the one-CTA kernel
+    for cl in (4, 1, 2, 0):  # speculative scan, cluster (partials pushed / pulled), one CTA
         eng.lib.snn_set_normad_cluster(cl)
         try:
             res.append(sd.train_epoch(ims, labs, sd.zero_weights(), bank, cfg, learn)[0])
         finally:
-            eng.lib.snn_set_normad_cluster(1)
+            eng.lib.snn_set_normad_cluster(_native.NORMAD_DEFAULT)
+    assert np.array_equal(res[0], res[1])  # speculative scan proven or redone: bit for bit
+    res = res[1:]
     assert np.array_equal(res[0], res[1])  # push and pull: same sums in the same order
     rel = np.abs(res[0] - res[2]).max() / np.abs(res[2]).max()
     assert rel <= 1e-12, rel   # G summed per shard vs sequentially: last-bit differences only

@@ -10,6 +10,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
+from paper_1711_03637_b200 import _native  # noqa: E402
 if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
@@ -289,8 +290,8 @@ def test_guard_band_hidden_kernel_bit_identical(sd, cfg, bank, workloads, wfix):
 
 
 def test_speculative_normad_bit_identical(sd, cfg, bank, workloads):
-    """The speculative-scan NormAD kernel (snn_set_normad_cluster(4),
-    normad_spec.cuh) runs image i+1's output scan on the sums of the weights
+    """The speculative-scan NormAD kernel (snn_set_normad_cluster(4), the
+    default; normad_spec.cuh) runs image i+1's output scan on the sums of the weights
     before image i's update and proves it (or redoes it): its weights and
     per-image counts equal the plain cluster kernel's bit for bit, and
     d_status[3] counts the redone scans."""
@@ -310,7 +311,7 @@ def test_speculative_normad_bit_identical(sd, cfg, bank, workloads):
             eng.stream.synchronize()
             res[mode] = (w.cpu().numpy(), cnt.cpu().numpy(), status.cpu().numpy())
         finally:
-            eng.lib.snn_set_normad_cluster(1)
+            eng.lib.snn_set_normad_cluster(_native.NORMAD_DEFAULT)
     assert np.array_equal(res[3][0], res[4][0])
     assert np.array_equal(res[3][1], res[4][1])
     assert res[4][2][0] == 0 and res[4][2][2] == n
