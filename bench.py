@@ -624,7 +624,7 @@ def kernel_table(stage_ms, call_ms, hidden_frac):
     bounds = {"k_prep": "hbm/latency (one pass over the images)", "k_tile_scan": "latency (one CTA)",
               "k_hidden_gb": "ALU pipe / issue (float32 pairs + integer decisions)",
               "k_hidden_fix": "fp64 dependent chain per flagged window (latency)",
-              "k_hidden_res": "fp64 pipe", "k_gsum": "issue / L2 gathers (W rows)",
+              "k_hidden_res": "fp64 pipe", "k_gsum": "L1 data pipe / issue (step lists, W-row gathers)",
               "k_output": "fp64 dependent chain per image (latency)"}
     out = {}
     for k, ms in stage_ms.items():
@@ -641,8 +641,12 @@ def kernel_table(stage_ms, call_ms, hidden_frac):
             if n and n.get("alu_pipe_pct") is not None:
                 e["ncu_alu_pipe_frac"] = n["alu_pipe_pct"] / 100.0
         elif k == "k_gsum" and n:
-            e["frac"] = (n.get("issue_active_pct") or 0) / 100.0
-            e["frac_basis"] = "issue slots busy (ncu smsp__issue_active); DRAM is dram_frac_of_hbm_peak"
+            iss, l1 = (n.get("issue_active_pct") or 0) / 100.0, (n.get("l1_wavefronts_pct") or 0) / 100.0
+            e["frac"] = max(iss, l1)
+            e["bound"] = ("L1 data pipe (step-list and W-row gather wavefronts)" if l1 >= iss
+                          else "issue (list building, W-row gathers)")
+            e["frac_basis"] = ("the busier of the L1 data-pipe wavefronts and the issue slots (ncu); DRAM is "
+                               "dram_frac_of_hbm_peak")
         elif k == "k_output" and n:
             fp, iss = (n.get("fp64_pipe_pct") or 0) / 100.0, (n.get("issue_active_pct") or 0) / 100.0
             e["frac"] = max(fp, iss)
@@ -726,28 +730,30 @@ def train_launches(eng, c, n):
 
 
 def critical_path_model(c):
-    """Per-image latency floor of the sequential NormAD chain:
-    the output scan's dependent chain per step (no output spike: 6 FP64 ops
-    of 8.2 cycles + threshold test, ballot and select ~25 cycles; after an
+    """Per-image latency floor of the sequential NormAD chain (DESIGN.md 4,
+    4.1): the output scan's dependent chain per step (no output spike: 6 FP64
+    ops of 8.2 cycles + threshold test, ballot and select ~25 cycles; after an
     output spike, 23% of steps, + bumps, difference and the 5-level pairwise
-    sum: 8 more FP64 ops) and the R adjoint's (DMUL -> DADD per step), at the
-    max SM clock; cluster barriers, the DSMEM gather and dW are not counted.
-    Latencies from scripts/scan_micro.py (FP64 dependent op 8.2 cycles)."""
+    sum: 8 more FP64 ops) at the max SM clock.  In the speculative kernel (the
+    default) the R adjoint, dW, the partial sums and the proof bound run on
+    the other warps under the next image's scan, so the chain is the scan;
+    cluster barriers and the check are not counted.  Latencies from
+    scripts/scan_micro.py (FP64 dependent op 8.2 cycles)."""
     n = c.n_steps
     lat = 8.2
     scan = 0.77 * (6 * lat + 25) + 0.23 * (14 * lat + 25)
     adj = 2 * lat
-    cyc = n * (scan + adj)
-    return {"model_us_per_image": cyc / 1965.0, "scan_cycles_per_step": scan, "adjoint_cycles_per_step": adj,
-            "n_steps": n, "clock_mhz": 1965,
-            "basis": "dependent-chain latency only (FP64 8.2 cycles); measured scan alone: 232 cycles/step "
-                     "(issue-bound single warp, scripts/scan_micro.py)"}
+    cyc = n * scan
+    return {"model_us_per_image": cyc / 1965.0, "scan_cycles_per_step": scan,
+            "adjoint_cycles_per_step_off_chain": adj, "n_steps": n, "clock_mhz": 1965,
+            "basis": "dependent-chain latency only (FP64 8.2 cycles); measured scan: 228 cycles/step, issue-bound "
+                     "single warp of ~160 instructions per step (scripts/scan_stamps.py)"}
 
 
 def train_kernel_table():
     """The training kernels' bounds and the fraction of each, from the newest
-    committed ncu capture (profiles/<round>_kernels.json): k_normad_cl is the
-    sequential chain (its fraction is the dependent-chain model over the
+    committed ncu capture (profiles/<round>_kernels.json): k_normad_spec (or
+    k_normad_cl when the speculative kernel is off) is the sequential chain (its fraction is the dependent-chain model over the
     measured time per image, critical_path.frac_of_measured); k_compact and
     k_shard are the W-independent preparation, overlapped with the chain on
     an auxiliary stream (issue slots busy)."""
@@ -755,11 +761,15 @@ def train_kernel_table():
     out = {}
     for name, recs in prof.items():
         k = _short(name)
-        if k in ("k_compact", "k_shard", "k_normad_cl"):
+        if k in ("k_compact", "k_shard", "k_normad_cl", "k_normad_spec"):
             r = recs[0]
             e = {"ncu": {x: r.get(x) for x in ("duration_ms", "issue_active_pct", "fp64_pipe_pct", "alu_pipe_pct",
                                               "dram_bytes") if r.get(x) is not None}}
-            if k == "k_normad_cl":
+            if k == "k_normad_spec":
+                e["bound"] = ("latency: one-warp output scan per image (8 of 148 SMs); the update of the "
+                              "previous image runs under it on the other warps")
+                e["frac_basis"] = "critical_path.frac_of_measured"
+            elif k == "k_normad_cl":
                 e["bound"] = "latency: one-warp output scan + adjoint recursion per image (8 of 148 SMs)"
                 e["frac_basis"] = "critical_path.frac_of_measured"
             else:

@@ -1253,8 +1253,12 @@ __device__ __forceinline__ DistK dist_k(const snn_consts_t &c) {
 
 // Advances one step given G (sum of W rows of hidden neurons spiking now).
 // Returns whether this lane's output neuron l fired; *ff_out = c_hidden @ W.
+// MARGIN (the speculative NormAD scan, normad_spec.cuh): *margin = the
+// candidate potential's distance to the threshold when the neuron is live,
+// +inf otherwise.
+template <bool MARGIN = false>
 __device__ __forceinline__ bool dist_step(DistState &st, const DistK &k, double G, int s, int l, int lane,
-                                         double *ff_out) {
+                                         double *ff_out, double *margin = nullptr) {
     st.Af = __dadd_rn(__dmul_rn(st.Af, k.lam1), G);
     st.Bf = __dadd_rn(__dmul_rn(st.Bf, k.lam2), G);
     const double ff = __dsub_rn(st.Af, st.Bf);
@@ -1309,6 +1313,7 @@ __device__ __forceinline__ bool dist_step(DistState &st, const DistK &k, double 
     const double vn = __dadd_rn(st.v, t);
     const bool live = s >= st.live_from;
     const bool fired = live && vn >= k.vt;
+    if (MARGIN) *margin = live ? fabs(vn - k.vt) : __longlong_as_double(0x7ff0000000000000LL);
     st.v = (!live || fired || vn < k.el) ? k.el : vn;
     if (fired) st.live_from = next_live_step(s, k.refr);
     st.prev = __ballot_sync(kFull, fired) & 0x3FFu;

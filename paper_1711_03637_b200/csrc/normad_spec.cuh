@@ -120,9 +120,52 @@ __device__ __forceinline__ bool outd_step_m(OutD &X, const snn_consts_t &c, doub
 #else
 #define SNN_SCAN_INLINE __forceinline__
 #endif
+#ifdef SNN_SPEC_SCAN_DIST
+// Lane-distributed step (measured slower: 268 against 228 cycles per step,
+// the candidate store -> load -> pairwise sum latency is on the chain;
+// DESIGN.md 9): dist_step (hidden.cuh: each lane owns one output's
+// inhibition traces; the ten candidates of the next step's sum go through a
+// 512-byte shared buffer), the same float64 operations as outd_step, so the
+// same bits, with half the FP64 instructions per lane of the replicated
+// step below.  dspec: 512-byte aligned.
 template <bool MARGIN>
 __device__ SNN_SCAN_INLINE int spec_scan(const snn_consts_t &c, const double *G, uint16_t *om, int N,
-                                         double *M, long long *stp = nullptr) {
+                                         double *M, char *dspec, long long *stp = nullptr) {
+    const int lane = threadIdx.x & 31;
+    const int l = lane < kNO ? lane : kNO - 1;
+    DistState st;
+    dist_init(st, c, dspec, lane);
+    // register copies of the constants, passed through a shuffle so ptxas
+    // cannot re-read them from the constant bank inside the loop (under this
+    // kernel's uniform-register pressure it otherwise reloads them on the
+    // step's dependency chain)
+    DistK k = dist_k(c);
+    {
+        double *v[8] = {&k.lam1, &k.lam2, &k.inh, &k.el, &k.vt, &k.g, &k.beta, &k.refr};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) *v[q] = __shfl_sync(kFull, *v[q], 0);
+    }
+    const double *gp = G + l;
+    for (int s = 0; s < N; ++s) {
+#ifdef SNN_SCAN_STAMPS
+        if (stp && lane == 0) stp[s] = clock64();
+#endif
+        double ff, m;
+        dist_step<MARGIN>(st, k, gp[s * kNO], s, l, lane, &ff, &m);
+        // unconditional stores (lanes >= kNO repeat lane kNO - 1's values; om[s]
+        // is the same ballot in every lane): no branch inside the step
+        if (MARGIN) M[s * kNO + l] = m;
+        om[s] = (uint16_t)st.prev;
+    }
+#ifdef SNN_SCAN_STAMPS
+    if (stp && lane == 0) stp[N] = clock64();
+#endif
+    return st.cnt;
+}
+#else
+template <bool MARGIN>
+__device__ SNN_SCAN_INLINE int spec_scan(const snn_consts_t &c, const double *G, uint16_t *om, int N,
+                                         double *M, char *, long long *stp = nullptr) {
     const int lane = threadIdx.x & 31;
     const int l = lane < kNO ? lane : kNO - 1;
     // Register copies of the constants a step reads, passed through a shuffle
@@ -175,6 +218,8 @@ __device__ SNN_SCAN_INLINE int spec_scan(const snn_consts_t &c, const double *G,
     return X.o.cnt;
 }
 
+#endif
+
 __device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 // Workers: the warps of scheduler partitions 1..3 (warp % 4 != 0), so the scan
@@ -224,6 +269,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
     double *Mg = Gx + g;                                                   // leader: |vn - V_T| of the scan
     double *Eb = Mg + g;                                                   // leader: the bound E
     __shared__ ClBuf s_buf[kSpBufs];
+    __shared__ __align__(512) char s_dspec[kDistSpecBytes];  // the scan warp's dist_step buffers
     __shared__ int s_abort, s_label, s_bad;
 
     const int rows = cl_rows(r);
@@ -323,7 +369,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
         if (n > 1) gather(Pn, Gb, tid, kSpThreads);  // G'_1: buffer 1 & 1 ^ 1 = 0
         cta_sync<6>();
         if (warp == 0) {
-            const int cnt = spec_scan<false>(c, Gx, OM, N, nullptr);
+            const int cnt = spec_scan<false>(c, Gx, OM, N, nullptr, s_dspec);
             if (lane < kNO) T.counts[lane] = cnt;
         }
         cta_sync<7>();
@@ -366,9 +412,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
 #ifndef SNN_SPEC_NOSPEC
 #ifdef SNN_SCAN_STAMPS
             if (r == 0 && spec && warp == 0)
-                cnt = spec_scan<true>(c, Gs, OMs, N, Mg, T.first + i + 1 == SNN_SCAN_STAMPS ? g_scan_stamps : nullptr);
+                cnt = spec_scan<true>(c, Gs, OMs, N, Mg, s_dspec, T.first + i + 1 == SNN_SCAN_STAMPS ? g_scan_stamps : nullptr);
 #else
-            if (r == 0 && spec && warp == 0) cnt = spec_scan<true>(c, Gs, OMs, N, Mg);
+            if (r == 0 && spec && warp == 0) cnt = spec_scan<true>(c, Gs, OMs, N, Mg, s_dspec);
 #endif
 #endif
             SP_STAMP(0, 1)
@@ -559,7 +605,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
 #endif
             fail = cta_sync_or<3>(fail);
             if (warp == 0) {
-                if (fail) cnt = spec_scan<false>(c, Gx, OMs, N, nullptr);  // redo on the exact G_{i+1}
+                if (fail) cnt = spec_scan<false>(c, Gx, OMs, N, nullptr, s_dspec);  // redo on the exact G_{i+1}
                 if (lane < kNO) T.counts[(size_t)(i + 1) * kNO + lane] = cnt;
                 if (lane == 0 && fail) atomicAdd(&T.status[3], 1);
             }

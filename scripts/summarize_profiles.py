@@ -36,6 +36,7 @@ METRICS = [
     ("dram__bytes_write.sum", "DRAM write"),
     ("lts__t_bytes.sum", "L2 bytes"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "L1 data-pipe wavefronts % of peak"),
 ]
 
 
@@ -76,7 +77,8 @@ def summarize(rep, fh, traffic, kernels=None):
                    "fma_pipe_pct": get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
                    "warps_active_per_sm": get("sm__warps_active.avg.per_cycle_active"),
                    "registers": get("launch__registers_per_thread"),
-                   "warp_instructions": get("smsp__inst_executed.sum")}
+                   "warp_instructions": get("smsp__inst_executed.sum"),
+                   "l1_wavefronts_pct": get("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed")}
             if "dram__bytes_read.sum" in h and "dram__bytes_write.sum" in h:
                 ir, iw = h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
                 rec["dram_bytes"] = _bytes(r[ir], units[ir]) + _bytes(r[iw], units[iw])
