@@ -42,7 +42,7 @@ __host__ __device__ inline size_t normad_spec_smem_bytes(int N) {
     const size_t g = (size_t)N * kNO * 8;
     return (size_t)kClRows * kNO * 8           // W shard
            + 3 * g                             // P (G_{i+1} partial), Pn (G'_{i+2} partial), SR (sigma -> R)
-           + (size_t)((N + 1) & ~1) * 8        // Q
+           + 2 * (size_t)((N + 1) & ~1) * 8    // Q double buffer (image parity)
            + 2 * (size_t)((N + 7) & ~7) * 2    // OMASK double buffer
            + 64 + 16                           // flags
            + kSpBufs * ((cl_buf_bytes(N) + 15) & ~(size_t)15)
@@ -255,8 +255,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
     double *P = Wsh + (size_t)kClRows * kNO;         // [N][10] this shard's partial of G_{i+1} (W_{i+1})
     double *Pn = P + g;                              // [N][10] this shard's partial of G'_{i+2} (W_{i+1})
     double *SR = Pn + g;                             // [N][10] sigma -> R
-    double *Q = SR + g;                              // [N] dt / |d_hat|
-    uint16_t *OM = reinterpret_cast<uint16_t *>(Q + ((N + 1) & ~1));  // [2][N8] output spikes, by image parity
+    const int QN = (N + 1) & ~1;
+    double *Qb = SR + g;                             // [2][QN] dt / |d_hat|, by image parity
+    uint16_t *OM = reinterpret_cast<uint16_t *>(Qb + 2 * QN);  // [2][N8] output spikes, by image parity
     const int N8 = (N + 7) & ~7;
     int *flags = reinterpret_cast<int *>(OM + 2 * N8);  // leader: per-CTA non-finite flags
     uint8_t *bufmem = reinterpret_cast<uint8_t *>(flags + 16);
@@ -270,7 +271,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
     double *Eb = Mg + g;                                                   // leader: the bound E
     __shared__ ClBuf s_buf[kSpBufs];
     __shared__ __align__(512) char s_dspec[kDistSpecBytes];  // the scan warp's dist_step buffers
-    __shared__ int s_abort, s_label, s_bad;
+    __shared__ int s_abort, s_bad, s_lab[2];
 
     const int rows = cl_rows(r);
     if (T.status[0] != 0) return;  // an earlier chunk failed (uniform over the cluster)
@@ -357,6 +358,20 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
             dst[t] = gs;
         }
     };
+    // the leader's scan warp: an image's output spikes (one OMASK parity
+    // buffer) into the other CTAs' copies, as 32-bit pairs
+    // (16-byte remote stores: each DSMEM store is one transaction of the SM's
+    // memory pipe, so fewer and wider ones keep it free for the check's loads)
+    auto push_om = [&](const uint16_t *om) {
+        __syncwarp();  // every lane's om stores are visible to the warp
+        const int nw = N8 / 8;
+        const uint4 *src = reinterpret_cast<const uint4 *>(om);
+        const int base = (int)(om - OM) / 8;
+        for (int t = lane; t < (kCl - 1) * nw; t += 32) {
+            const int q = 1 + t / nw, w = t - (q - 1) * nw;
+            reinterpret_cast<uint4 *>(cluster.map_shared_rank(OM, q))[base + w] = src[w];
+        }
+    };
 
     // ---- prologue: lists of images 0..2, G_0 and G'_1 (both with W_0), scan of image 0
     for (int64_t j = 0; j < 3 && j < n; ++j) stage(j, (int)j, tid, kSpThreads);
@@ -379,8 +394,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
         }
     }
     if (n > 0) {
-        for (int s = tid; s < N; s += kSpThreads) Q[s] = SW.q[s];
-        if (tid == 0) s_label = T.labels[0];
+        for (int s = tid; s < N; s += kSpThreads) Qb[s] = SW.q[s];
+        if (tid == 0) s_lab[0] = T.labels[0];
     }
     cluster.sync();  // OMASK_0 everywhere; the leader is done reading P, Pn
 
@@ -416,6 +431,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
 #else
             if (r == 0 && spec && warp == 0) cnt = spec_scan<true>(c, Gs, OMs, N, Mg, s_dspec);
 #endif
+            if (r == 0 && spec && warp == 0) {  // final unless the check below fails
+                push_om(OMs);
+                if (lane < kNO) T.counts[(size_t)(i + 1) * kNO + lane] = cnt;
+            }
 #endif
             SP_STAMP(0, 1)
             cl_wait();
@@ -423,7 +442,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
             // ---- workers: image i's update, then the partials of images i+1 / i+2
             SP_STAMP(32, 14)
             {  // sigma (all workers), then R by the adjoint recursion of k_normad_cl (warp 1)
-                const int label = s_label;
+                const int label = s_lab[par];
+                const double *Q = Qb + par * QN;
                 const int per = c.desired_period;
                 for (int t = wt; t < N * kNO; t += kSpWorkers) {
                     const int s = t / kNO, l = t - s * kNO;
@@ -442,6 +462,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
                         pb = __dadd_rn(__dmul_rn(pb, c.decay_fast), q);
                         SR[u * kNO + lane] = __dsub_rn(pa, pb);
                     }
+                } else if (warp != 1 && spec) {
+                    // while warp 1 runs R: image i+1's gate values and label into the
+                    // other parity's buffers (iteration i-1 released them at its end)
+                    double *Qn = Qb + (par ^ 1) * QN;
+                    for (int s = wt - 32; s < N; s += kSpWorkers - 32) Qn[s] = SW.q[(size_t)(i + 1) * N + s];
+                    if (wt == 32) s_lab[par ^ 1] = T.labels[i + 1];
                 }
             }
             SP_STAMP(32, 15)
@@ -582,8 +608,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
         SP_STAMP(0, 11)
         cta_sync<2>();  // (1) the scan, E and the flags are done
         SP_STAMP(0, 8)
-        SP_STAMP(32, 12)
-        SP_STAMP(128, 13)
         if (s_abort) {  // image i produced a non-finite weight: undo it and stop
             for (int t = tid; t < Bi.n_act * kNO; t += kSpThreads) {
                 const int row = Bi.act[t / kNO];
@@ -603,25 +627,20 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSpThreads, 1)
 #ifdef SNN_SPEC_NOSPEC
             fail = 1;
 #endif
+            SP_STAMP(0, 12)
             fail = cta_sync_or<3>(fail);
-            if (warp == 0) {
-                if (fail) cnt = spec_scan<false>(c, Gx, OMs, N, nullptr, s_dspec);  // redo on the exact G_{i+1}
+            SP_STAMP(0, 13)
+            if (warp == 0 && fail) {  // redo on the exact G_{i+1}; its spikes and counts replace the speculative ones
+                cnt = spec_scan<false>(c, Gx, OMs, N, nullptr, s_dspec);
+                push_om(OMs);
                 if (lane < kNO) T.counts[(size_t)(i + 1) * kNO + lane] = cnt;
-                if (lane == 0 && fail) atomicAdd(&T.status[3], 1);
+                if (lane == 0) atomicAdd(&T.status[3], 1);
             }
-            cta_sync<4>();  // (2) OMs final
             SP_STAMP(0, 9)
-            for (int t = tid; t < (kCl - 1) * N; t += kSpThreads) {
-                const int q = 1 + t / N, s = t - (q - 1) * N;
-                cluster.map_shared_rank(OM, q)[(par ^ 1) * N8 + s] = OMs[s];
-            }
         }
-        // ---- image i is done; hand over to image i+1
+        // ---- image i is done; hand over to image i+1 (its gate values and
+        // label were prefetched by the workers)
         if (r == 0 && tid == 0) T.status[2] = (int32_t)(T.first + i + 1);
-        if (spec) {
-            for (int s = tid; s < N; s += kSpThreads) Q[s] = SW.q[(size_t)(i + 1) * N + s];
-            if (tid == 0) s_label = T.labels[i + 1];
-        }
         cluster.sync();  // OMASK_{i+1} everywhere; the leader is done reading P, Pn
         SP_STAMP(0, 10)
     }

@@ -23,7 +23,7 @@ for rep in range(3):
 eng.lib.snn_normad_phase_clocks(None)
 k = clk.cpu().numpy()[4:60].astype(np.float64)
 names = {1: "scan warp done", 2: "R + stage", 3: "dW", 4: "partials", 5: "barrier A", 6: "gathers",
-         7: "E bound", 8: "(1)", 9: "check (2)", 10: "handover"}
+         7: "E bound", 8: "(1)", 12: "check loop", 13: "check barrier", 9: "check (2)", 10: "handover"}
 print("cycles since loop top (median over images 4..59):")
 for j, nm in names.items():
     print(f"  {nm:16s} {np.median(k[:, j] - k[:, 0]):8.0f}")
