@@ -74,7 +74,13 @@ struct BatchArgs {
     double *gabs;            // [n][N][10] |W| sums (near_ties only)
     int32_t *fix_count;      // guard-band hidden layer (hidden_gb.cuh): flagged windows
     int32_t *fix_list;       // [n * 676] their indices in the compacted window list
+    double *wpad;            // [8112][16] W rows padded to 128 bytes (k_prep -> k_gsum), or null
 };
+
+// W row stride of the contraction's gathers: 16 doubles (one 128-byte line per
+// row, copied by k_prep) for large batches, the caller's 10 otherwise
+constexpr int kWPad = 16;
+constexpr int kWPadMinImages = 256;
 
 __device__ __forceinline__ uint64_t warp_excl_scan_u64(uint64_t x, uint64_t *total) {
     const int lane = threadIdx.x & 31;
@@ -119,6 +125,11 @@ __global__ void __launch_bounds__(kThreads) k_prep(const BatchArgs A) {
     const int64_t img = blockIdx.x;
     const uint8_t *gimg = A.images + img * (kSide * kSide);
     if (tid < 49) reinterpret_cast<uint4 *>(s_img)[tid] = __ldg(reinterpret_cast<const uint4 *>(gimg) + tid);
+    if (A.wpad)  // the contraction's padded W rows: a few pairs per CTA
+        for (int64_t t = img * kThreads + tid; t < kNH * kNO / 2; t += (int64_t)gridDim.x * kThreads) {
+            const int row = (int)(t / (kNO / 2)), q = (int)(t - (int64_t)row * (kNO / 2));
+            reinterpret_cast<double2 *>(A.wpad + (size_t)row * kWPad)[q] = __ldg(reinterpret_cast<const double2 *>(A.w) + t);
+        }
     // Skipping all-zero windows is exact only while pixel level 0 never
     // spikes (its input trace, table column 0, stays +0).  The reference
     // accepts i_0 within rel_tol 1e-9 of the rheobase (network.py:133-136),
@@ -895,7 +906,7 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t x) {
 // round hit distinct banks; rows stay 16-byte aligned for the 8-id loads.
 template <int CAP>
 constexpr int ids_stride() { return CAP + 8; }
-static_assert(kNO % 2 == 0 && kNH * (kNO / 2) <= 0xFFFF, "list entries: W row offsets in double2 units fit 16 bits");
+static_assert(kNO % 2 == 0 && kNH * (kWPad / 2) <= 0xFFFF, "list entries: W row offsets in double2 units fit 16 bits");
 
 template <int CAP>
 struct GsumSmem {
@@ -907,7 +918,7 @@ struct GsumSmem {
 // ABS (near-tie accounting only, snn_infer_out_t.near_ties): also Gabs(s, l) =
 // sum of |W[k, l]| over the same spikes, the magnitude the rounding bound of
 // k_output<TIES> needs.
-template <int CAP, bool ABS = false>
+template <int CAP, bool ABS = false, int WS = kNO>
 __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double *Gabs, int64_t img, int ch,
                                           GsumSmem<CAP> &S) {
     const int kStepCap = CAP;
@@ -919,7 +930,7 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
     for (int k = lane; k < nt * kTile; k += 32) S.pos[k] = A.tile_pos[img * (kMaxTiles * kTile) + k];
     const uint16_t *PP = S.pos;
     const uint8_t *R = A.raster + raster_tc(A.tile_base[img], nch, nt, ch, 0) + lane * kChunk;
-    const double *W = A.w;
+    const double *W = WS == kNO ? A.w : A.wpad;  // row stride WS doubles
     // ---- lists: lane (jl, g) = (step, window group of 8)
     const int jl = lane >> 2, g = lane & 3;
     uint32_t runl = 0;  // step jl's list length so far
@@ -989,7 +1000,7 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
             uint32_t w = wq[q];
             if (w) {
                 // list entries are W row offsets in double2 units: neuron id * kNO / 2
-                constexpr int kR = kNO / 2;
+                constexpr int kR = WS / 2;
                 // b = 16 plane + 8 window + feature-in-plane t:
                 // id * kR = r_window + kR t + kHalf kR plane = kR b + r'_window - (16 - kHalf) kR plane
                 const int r0 = (int)tp[8 * q] * (kNF * kR), r1 = (int)tp[8 * q + 4] * (kNF * kR) - 8 * kR;
@@ -1071,7 +1082,7 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
             __syncwarp();
             if (lane < kNO)
                 for (int e = 0; e < tt; ++e) {
-                    const double wv = __ldg(W + (size_t)S.ids[e] * kNO + lane);
+                    const double wv = __ldg(W + (size_t)S.ids[e] * WS + lane);
                     g = __dadd_rn(g, wv);
                     if (ABS) ga += fabs(wv);
                 }
@@ -1087,7 +1098,7 @@ __device__ __forceinline__ void gsum_task(const BatchArgs &A, double *G, double 
 #ifndef SNN_GSUM_MINB
 #define SNN_GSUM_MINB 10
 #endif
-template <bool ABS>
+template <bool ABS, int WS = kNO>
 __global__ void __launch_bounds__(kGWarps * 32, SNN_GSUM_MINB) k_gsum(const BatchArgs A, double *G, double *Gabs) {
     __shared__ __align__(16) GsumSmem<kStepCap> smem[kGWarps];
     const int warp = threadIdx.x >> 5;
@@ -1095,7 +1106,7 @@ __global__ void __launch_bounds__(kGWarps * 32, SNN_GSUM_MINB) k_gsum(const Batc
     const int64_t task = (int64_t)blockIdx.x * kGWarps + warp;
     if (task >= A.n_images * nch) return;
     const int64_t img = task / nch;
-    gsum_task<kStepCap, ABS>(A, G, Gabs, img, (int)(task - img * nch), smem[warp]);
+    gsum_task<kStepCap, ABS, WS>(A, G, Gabs, img, (int)(task - img * nch), smem[warp]);
 }
 
 // ---------------------------------------------------------------------------

@@ -67,6 +67,7 @@ struct InferWS {
     double *g;     // [n][N][10] G rows (k_gsum -> k_output)
     double *gabs;  // [n][N][10] sum of |W| rows (near-tie accounting only)
     int32_t *fix;  // [1 + n * 676] guard-band hidden layer: count, flagged windows
+    double *wpad;  // [8112][16] padded W rows for k_gsum (batches of >= kWPadMinImages), else null
 };
 
 size_t infer_ws_layout(const snn_consts_t *c, int64_t n, char *base, InferWS *w) {
@@ -86,6 +87,7 @@ size_t infer_ws_layout(const snn_consts_t *c, int64_t n, char *base, InferWS *w)
     x.g = (double *)take((size_t)n * c->n_steps * kNO * 8);
     x.gabs = (double *)take((size_t)n * c->n_steps * kNO * 8);
     x.fix = (int32_t *)take(((size_t)n * kNPos + 1) * 4);
+    x.wpad = n >= kWPadMinImages ? (double *)take((size_t)kNH * kWPad * 8) : nullptr;
 
     if (w) *w = x;
     return off;
@@ -350,7 +352,9 @@ int launch_contract(const BatchArgs &A, double *g, cudaStream_t st) {
     const int64_t tasks = n * n_chunks(A.c.n_steps);
     const unsigned gg = (unsigned)((tasks + kGWarps - 1) / kGWarps), og = (unsigned)((n + kOutWarps2 - 1) / kOutWarps2);
     double *gabs = A.out.near_ties ? A.gabs : nullptr;
-    if (gabs) k_gsum<true><<<gg, kGWarps * 32, 0, st>>>(A, g, gabs);
+    if (gabs && A.wpad) k_gsum<true, kWPad><<<gg, kGWarps * 32, 0, st>>>(A, g, gabs);
+    else if (gabs) k_gsum<true><<<gg, kGWarps * 32, 0, st>>>(A, g, gabs);
+    else if (A.wpad) k_gsum<false, kWPad><<<gg, kGWarps * 32, 0, st>>>(A, g, nullptr);
     else k_gsum<false><<<gg, kGWarps * 32, 0, st>>>(A, g, nullptr);
     if ((rc = cuda_check("k_gsum"))) return rc;
     stage_mark(4, st);
@@ -502,6 +506,7 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
     A.gabs = w.gabs;
     A.fix_count = w.fix;
     A.fix_list = w.fix + 1;
+    A.wpad = w.wpad;
 
     A.out = *out;
     const bool def = is_default_bank(*c);
@@ -536,6 +541,7 @@ extern "C" int snn_infer(const snn_consts_t *c, const uint8_t *d_images, int64_t
         if (out->v_out) B.out.v_out = out->v_out + i0 * N * kNO;
         if (out->near_ties) B.out.near_ties = out->near_ties + i0;
         B.gabs = w.gabs + (size_t)i0 * N * kNO;
+        B.wpad = nullptr;  // sub-batches overlap: each one's k_gsum reads the caller's W
         if ((rc = def ? launch_hidden_fast<true>(B, s) : launch_hidden_fast<false>(B, s))) return rc;
         cudaEventRecord(pp->ev[b], s);
         cudaStreamWaitEvent(pp->aux, pp->ev[b], 0);
