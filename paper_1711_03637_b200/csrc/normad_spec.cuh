@@ -162,6 +162,77 @@ __device__ SNN_SCAN_INLINE int spec_scan(const snn_consts_t &c, const double *G,
 #endif
     return st.cnt;
 }
+#elif defined(SNN_SPEC_SCAN_GATHER)
+// Lane-owned traces with the ten values of each pairwise sum gathered by
+// shuffles (no shared-memory round trip): the same float64 operations, in the
+// same order, as outd_step_m, so the same bits; 12 instead of ~39 FP64
+// instructions per lane for the sums.
+__device__ __forceinline__ double pairwise10_lanes(double x) {
+    double v[kNO];
+#pragma unroll
+    for (int j = 0; j < kNO; ++j) v[j] = __shfl_sync(kFull, x, j);
+    return pairwise10(v);
+}
+
+template <bool MARGIN>
+__device__ SNN_SCAN_INLINE int spec_scan(const snn_consts_t &c, const double *G, uint16_t *om, int N,
+                                         double *M, char *, long long *stp = nullptr) {
+    const int lane = threadIdx.x & 31;
+    const int l = lane < kNO ? lane : kNO - 1;
+    double lam1 = c.decay_slow, lam2 = c.decay_fast, inh = c.inhibition, el = c.lif_out.el, vt = c.lif_out.vt,
+           gl = c.lif_out.g, beta = c.lif_out.beta, refr = c.lif_out.refr;
+    {
+        double *v[8] = {&lam1, &lam2, &inh, &el, &vt, &gl, &beta, &refr};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) *v[q] = __shfl_sync(kFull, *v[q], 0);  // opaque to ptxas
+    }
+    const double *gp = G + l;
+    double al = 0.0, bl = 0.0;  // this lane's output traces times their decay
+    double Af = __dadd_rn(__dmul_rn(0.0, lam1), gp[0]), Bf = __dadd_rn(__dmul_rn(0.0, lam2), gp[0]);
+    double D0 = __dadd_rn(__dsub_rn(Af, Bf), __dmul_rn(inh, __dsub_rn(0.0, 0.0)));
+    double v = el;
+    int live_from = 0, cnt = 0;
+    unsigned prev = 0u;
+    for (int s = 0; s < N; ++s) {
+#ifdef SNN_SCAN_STAMPS
+        if (stp && lane == 0) stp[s] = clock64();
+#endif
+        const double Gn = gp[(s + 1 < N ? s + 1 : s) * kNO];
+        double a = al, b = bl, drive = D0;
+        if (prev != 0u) {
+            const double bump = ((prev >> l) & 1u) ? 1.0 : 0.0;
+            a = __dadd_rn(al, bump);
+            b = __dadd_rn(bl, bump);
+            const double cc = __dsub_rn(a, b);
+            const double S = pairwise10_lanes(cc);
+            drive = __dadd_rn(__dsub_rn(Af, Bf), __dmul_rn(inh, __dsub_rn(S, cc)));
+        }
+        double t = __dsub_rn(v, el);
+        t = __dmul_rn(gl, t);
+        t = __dsub_rn(drive, t);
+        t = __dmul_rn(beta, t);
+        const double vn = __dadd_rn(v, t);
+        const bool live = s >= live_from;
+        const bool fired = live && vn >= vt;
+        if (MARGIN) M[s * kNO + l] = live ? fabs(vn - vt) : __longlong_as_double(0x7ff0000000000000LL);
+        v = (!live || fired || vn < el) ? el : vn;
+        if (fired) live_from = next_live_step(s, refr);
+        prev = __ballot_sync(kFull, fired) & 0x3FFu;
+        cnt += fired ? 1 : 0;
+        al = __dmul_rn(a, lam1);
+        bl = __dmul_rn(b, lam2);
+        const double c0 = __dsub_rn(al, bl);
+        const double S0 = pairwise10_lanes(c0);
+        Af = __dadd_rn(__dmul_rn(Af, lam1), Gn);
+        Bf = __dadd_rn(__dmul_rn(Bf, lam2), Gn);
+        D0 = __dadd_rn(__dsub_rn(Af, Bf), __dmul_rn(inh, __dsub_rn(S0, c0)));
+        om[s] = (uint16_t)prev;
+    }
+#ifdef SNN_SCAN_STAMPS
+    if (stp && lane == 0) stp[N] = clock64();
+#endif
+    return cnt;
+}
 #else
 template <bool MARGIN>
 __device__ SNN_SCAN_INLINE int spec_scan(const snn_consts_t &c, const double *G, uint16_t *om, int N,
