@@ -55,9 +55,19 @@ def _to_device(eng, arr: np.ndarray):
         return t.to(eng.device, non_blocking=True)
 
 
-def _fetch(eng, t) -> np.ndarray:
+def _fetch(eng, t, dtype=None) -> np.ndarray:
+    """Device tensor -> a fresh host array (converted to dtype if given),
+    through the engine's pinned staging buffer: one DMA on the engine stream,
+    no pageable bounce.  The caller holds eng.lock (the buffer is shared)."""
+    import torch
+    nb = t.numel() * t.element_size()
+    buf = eng.pinned("fetch", nb)
+    host = buf[:nb].view(t.dtype).view(t.shape)
+    with torch.cuda.stream(eng.stream):
+        host.copy_(t, non_blocking=True)
     eng.stream.synchronize()
-    return t.cpu().numpy()
+    a = host.numpy()
+    return a.astype(dtype) if dtype is not None else a.copy()
 
 
 def decode_hidden(raster: np.ndarray, tile_base: int, tile_pos: np.ndarray, n_tiles: int,
@@ -131,7 +141,7 @@ def run_presentation(image, weights, filters, cfg,
         d_img = _to_device(eng, img.reshape(1, -1))
         d_w = _to_device(eng, w)
         out = eng.infer(c, d_img, d_w, raster=record)
-        counts = _fetch(eng, out["counts"])[0].astype(np.int64)
+        counts = _fetch(eng, out["counts"][0], np.int64)
         if record:
             raster = out["raster"].cpu().numpy()
             tpos = out["tile_pos"][0].cpu().numpy()
@@ -158,7 +168,7 @@ def forward_pass(image, weights, filters, cfg):
     c = make_consts(cfg, filters)
     with eng.lock:
         _, spk = eng.table(c)
-        spk = _fetch(eng, spk).astype(bool)
+        spk = _fetch(eng, spk, bool)
     per_level = [np.flatnonzero(spk[:, k]).tolist() for k in range(256)]
     return _SPIKE_RECORD(
         input_spikes=[list(per_level[k]) for k in levels.ravel()],
@@ -187,7 +197,7 @@ def batch_counts(images, weights, filters, cfg, workers: int = 1) -> np.ndarray:
         d_w = eng.weights(weights, check=_weights)   # validated once per distinct W, kept on the device
         d_img = eng.upload("images", imgs).view(len(imgs), -1)
         counts = eng.infer(c, d_img, d_w)["counts"]
-        return _fetch(eng, counts).astype(np.int64)
+        return _fetch(eng, counts, np.int64)
 
 
 @dataclass
