@@ -1338,6 +1338,9 @@ __device__ __forceinline__ bool dist_step(DistState &st, const DistK &k, double 
 
 
 constexpr int kOutDistMinImages = 256;
+// OUTS: the optional per-step outputs (out_raster, ff, v_out) are requested;
+// without them the step loop carries no per-step branches or stores.
+template <bool OUTS>
 __global__ void __launch_bounds__(kOutWarps2 * 32) k_output_dist(const BatchArgs A, const double *G) {
     __shared__ __align__(16) double s_g[kOutWarps2][kOSteps * kNO];
     __shared__ __align__(512) char spec[kOutWarps2][kDistSpecBytes];
@@ -1350,7 +1353,12 @@ __global__ void __launch_bounds__(kOutWarps2 * 32) k_output_dist(const BatchArgs
     double *sg = s_g[warp];
     DistState st;
     dist_init(st, A.c, spec[warp], lane);
-    const DistK k = dist_k(A.c);
+    DistK k = dist_k(A.c);
+    {  // register copies (through a shuffle, so ptxas cannot re-read them from the constant bank in the loop)
+        double *v[8] = {&k.lam1, &k.lam2, &k.inh, &k.el, &k.vt, &k.g, &k.beta, &k.refr};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) *v[q] = __shfl_sync(kFull, *v[q], 0);
+    }
     for (int s0 = 0; s0 < N; s0 += kOSteps) {
         const int ns = min(kOSteps, N - s0);
         for (int q = lane; q < ns * kNO; q += 32) sg[q] = __ldcs(Gi + (size_t)s0 * kNO + q);
@@ -1359,10 +1367,12 @@ __global__ void __launch_bounds__(kOutWarps2 * 32) k_output_dist(const BatchArgs
             const int s = s0 + j;
             double ff;
             dist_step(st, k, sg[j * kNO + l], s, l, lane, &ff);
-            if (A.out.out_raster && lane == 0) A.out.out_raster[(size_t)img * N + s] = (uint16_t)st.prev;
-            if (lane < kNO) {
-                if (A.out.ff) A.out.ff[((size_t)img * N + s) * kNO + lane] = ff;
-                if (A.out.v_out) A.out.v_out[((size_t)img * N + s) * kNO + lane] = st.v;
+            if (OUTS) {
+                if (A.out.out_raster && lane == 0) A.out.out_raster[(size_t)img * N + s] = (uint16_t)st.prev;
+                if (lane < kNO) {
+                    if (A.out.ff) A.out.ff[((size_t)img * N + s) * kNO + lane] = ff;
+                    if (A.out.v_out) A.out.v_out[((size_t)img * N + s) * kNO + lane] = st.v;
+                }
             }
         }
         __syncwarp();

@@ -362,7 +362,10 @@ int launch_contract(const BatchArgs &A, double *g, cudaStream_t st) {
     // kernel is FP64-throughput bound there), small ones: the replicated step
     // (shorter serial chain per image)
     if (gabs) k_output<true><<<og, kOutWarps2 * 32, 0, st>>>(A, g, gabs);
-    else if (A.n_images >= kOutDistMinImages && knobs().out_dist) k_output_dist<<<og, kOutWarps2 * 32, 0, st>>>(A, g);
+    else if (A.n_images >= kOutDistMinImages && knobs().out_dist) {
+        if (A.out.out_raster || A.out.ff || A.out.v_out) k_output_dist<true><<<og, kOutWarps2 * 32, 0, st>>>(A, g);
+        else k_output_dist<false><<<og, kOutWarps2 * 32, 0, st>>>(A, g);
+    }
     else k_output<false><<<og, kOutWarps2 * 32, 0, st>>>(A, g, nullptr);
     stage_mark(5, st);
     return cuda_check("k_output");
