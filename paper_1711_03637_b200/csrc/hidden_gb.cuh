@@ -618,4 +618,73 @@ __global__ void __launch_bounds__(kFixThreads) k_hidden_fix(const BatchArgs A) {
     }
 }
 
+// The same redo with the whole [N][256] table resident in shared memory (one
+// cooperative load per CTA, N <= kResMaxSteps): no per-chunk copies or
+// barriers, so a window's 4 lanes run their N steps back to back.  512
+// threads per CTA, one CTA per SM; a CTA with no flagged window to take
+// returns before loading the table.
+constexpr int kFixResThreads = 512;
+template <bool SGN, int FZ>
+__global__ void __launch_bounds__(kFixResThreads, 1) k_hidden_fix_res(const BatchArgs A) {
+    extern __shared__ __align__(16) double rtab[];  // [N][256]
+    const int N = A.c.n_steps;
+    const int count = *A.fix_count;
+    if ((int64_t)blockIdx.x * kFixResThreads >= 4LL * count) return;  // CTA-uniform
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(A.ctab);
+        uint4 *dst = reinterpret_cast<uint4 *>(rtab);
+        for (int i = threadIdx.x; i < N * 128; i += kFixResThreads) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    const int nchunks = n_chunks(N);
+    const LifK ph = lif_k(A.c.lif_hid);
+    const int g = threadIdx.x & 3;
+    double ts[9], tc[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        ts[k] = c_fix_tap[g][k];
+        tc[k] = c_fix_tap[8 + g][k];
+    }
+    const int nthr = (int)(gridDim.x * kFixResThreads);
+    for (int tb = (int)(blockIdx.x * kFixResThreads); tb < 4 * count; tb += nthr) {  // CTA-uniform
+        const int t = (tb + (int)threadIdx.x) >> 2;  // this quad's window
+        const bool have = t < count;
+        ItemState it;
+        window_setup(A, have, have ? A.fix_list[t] : 0, 0, nchunks, it);
+        uint32_t off[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) off[k] = (it.lvp[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+        double v0 = A.c.lif_hid.el, v1 = v0, v2 = v0;
+        unsigned h0 = 0, h1 = 0, h2 = 0;
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const double *T = rtab + (size_t)ch * kChunk * 256;
+            const int nrows = min(kChunk, N - ch * kChunk);
+            uint64_t p0 = 0, p1 = 0;
+            for (int j = 0; j < nrows; ++j) {
+                double x[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) x[k] = T[j * 256 + off[k]];
+                double Is = __dmul_rn(x[0], ts[0]), Ic = __dmul_rn(x[0], tc[0]);
+#pragma unroll
+                for (int k = 1; k < 9; ++k) {
+                    Is = __fma_rn(x[k], ts[k], Is);
+                    Ic = __fma_rn(x[k], tc[k], Ic);
+                }
+                unsigned m = fix_lif<SGN, FZ>(Is, v0, h0, ph) ? 1u << g : 0u;
+                m |= fix_lif<SGN, FZ>(-Is, v1, h1, ph) ? 1u << (g + 4) : 0u;
+                m |= fix_lif<SGN, FZ>(Ic, v2, h2, ph) ? 1u << (g + 8) : 0u;
+                m |= __shfl_xor_sync(kFull, m, 1);
+                m |= __shfl_xor_sync(kFull, m, 2);
+                p0 |= (uint64_t)(m & 0x3Fu) << (8 * j);
+                p1 |= (uint64_t)(m >> kHalf) << (8 * j);
+            }
+            if (g == 0 && have && it.on) {
+                uint64_t *dst = reinterpret_cast<uint64_t *>(it.rout + (size_t)ch * it.rstride);
+                dst[0] = p0;
+                dst[kTile] = p1;
+            }
+        }
+    }
+}
+
 }  // namespace snn

@@ -271,7 +271,20 @@ int launch_hidden_gb(const BatchArgs &A, cudaStream_t st, int variant) {
     int rc = cuda_check("k_hidden_gb");
     if (rc) return rc;
     stage_mark(6, st);
-    k_hidden_fix<SGN, 3><<<(unsigned)(4 * sm_count()), kFixThreads, 0, st>>>(A);
+    if (A.c.n_steps <= kResMaxSteps) {  // table resident in shared memory
+        const size_t fsm = (size_t)A.c.n_steps * 256 * 8;
+        static int attr_set[kMaxDev] = {};
+        int &done = attr_set[cur_dev()];
+        if (done < (int)fsm) {
+            if (cudaFuncSetAttribute(k_hidden_fix_res<SGN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)fsm) != cudaSuccess)
+                return cuda_check("cudaFuncSetAttribute(k_hidden_fix_res)");
+            done = (int)fsm;
+        }
+        k_hidden_fix_res<SGN, 3><<<(unsigned)sm_count(), kFixResThreads, fsm, st>>>(A);
+    } else {
+        k_hidden_fix<SGN, 3><<<(unsigned)(4 * sm_count()), kFixThreads, 0, st>>>(A);
+    }
     if ((rc = cuda_check("k_hidden_fix"))) return rc;
     if (A.out.hidden_redo) cudaMemcpyAsync(A.out.hidden_redo, A.fix_count, 4, cudaMemcpyDeviceToDevice, st);
     return SNN_OK;
