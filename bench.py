@@ -629,7 +629,7 @@ def kernel_table(stage_ms, call_ms, hidden_frac):
     out = {}
     for k, ms in stage_ms.items():
         e = {"ms": ms, "share_of_call": ms / call_ms if call_ms else None, "bound": bounds.get(k)}
-        n = ncu.get(k) or (ncu.get("k_output_dist") if k == "k_output" else None)
+        n = ncu.get(k) or ncu.get({"k_output": "k_output_dist", "k_hidden_fix": "k_hidden_fix_res"}.get(k, ""))
         if n:
             e["ncu"] = {x: n.get(x) for x in ("issue_active_pct", "fp64_pipe_pct", "alu_pipe_pct", "fma_pipe_pct",
                                               "dram_bytes", "duration_ms") if n.get(x) is not None}
@@ -649,9 +649,12 @@ def kernel_table(stage_ms, call_ms, hidden_frac):
                                "dram_frac_of_hbm_peak")
         elif k == "k_output" and n:
             fp, iss = (n.get("fp64_pipe_pct") or 0) / 100.0, (n.get("issue_active_pct") or 0) / 100.0
-            e["frac"] = max(fp, iss)
-            e["bound"] = "issue (lane-distributed step, k_output_dist)" if iss >= fp else "fp64 pipe"
-            e["frac_basis"] = "the busier of the FP64 pipe and the issue slots (ncu); a warp is one image's serial chain"
+            l1 = (n.get("l1_wavefronts_pct") or 0) / 100.0
+            e["frac"] = max(fp, iss, l1)
+            e["bound"] = ("L1 data pipe (the lane-distributed step's candidate exchange, k_output_dist)" if l1 >= max(fp, iss)
+                          else "issue (lane-distributed step, k_output_dist)" if iss >= fp else "fp64 pipe")
+            e["frac_basis"] = ("the busiest of the L1 data pipe, the FP64 pipe and the issue slots (ncu); a warp is "
+                               "one image's serial chain")
         elif n:
             e["frac"] = (n.get("issue_active_pct") or 0) / 100.0
             e["frac_basis"] = "issue slots busy (ncu)"
