@@ -342,3 +342,33 @@ def test_output_dist_bit_identical(sd, cfg, bank, workloads, wfix):
     assert res[0][0].sum() > 0
     for a, b in zip(res[0], res[1]):
         assert np.array_equal(a, b)
+
+
+def test_guard_band_long_trial_chunked_redo(sd, cfg, bank, workloads, wfix):
+    """T = 150 ms (N = 150 > 108 steps: the float64 redo streams the table in
+    chunks, k_hidden_fix, instead of holding it in shared memory): the guard
+    band against the float64 ring kernel on 1,000 config-3 images -- counts
+    and the decoded hidden rasters of 40 of them."""
+    from paper_1711_03637_b200.api import decode_hidden
+    from paper_1711_03637_b200.engine import get_engine, make_consts
+    eng = get_engine()
+    c = make_consts(dataclasses.replace(cfg, t=0.15), bank)
+    assert c.n_steps == 150
+    n = 1000
+    imgs = torch.from_numpy(workloads["c3_images"][:n].reshape(n, -1).copy()).to(eng.device)
+    w = torch.from_numpy(wfix["w_fix"].copy()).to(eng.device)
+    res = {}
+    for mode in (1, 3):
+        eng.lib.snn_set_hidden_resident(mode)
+        try:
+            o = eng.infer(c, imgs, w, raster=True)
+            eng.stream.synchronize()
+            r, tb, tp, nt = (o[k].cpu().numpy() for k in ("raster", "tile_base", "tile_pos", "n_tiles"))
+            dec = np.stack([decode_hidden(r, int(tb[i]), tp[i], int(nt[i]), c.n_steps) for i in range(0, n, 25)])
+            res[mode] = (o["counts"].cpu().numpy(), dec, int(o["hidden_redo"].item()))
+        finally:
+            eng.lib.snn_set_hidden_resident(1)
+    assert res[1][2] > 0  # the guard band ran and flagged some windows
+    assert res[1][1].any()
+    assert np.array_equal(res[1][0], res[3][0])
+    assert np.array_equal(res[1][1], res[3][1])
