@@ -1,5 +1,5 @@
 """Median device time of the guard-band hidden layer and of its float64 redo
-(library stage events 2 -> 6 -> 3) over 20 calls of the 10,000-image c3 batch."""
+(library stage events 2 -> 6 -> 3) over 20 calls of an n-image c3 batch (argv[1], default 10,000)."""
 import ctypes, os, statistics, sys
 import numpy as np
 import torch
@@ -11,7 +11,8 @@ d = np.load(os.path.join(ROOT, "data", "workloads.npz"))
 eng = get_engine()
 c = make_consts(sd.NetworkConfig(), sd.default_filter_bank())
 w = torch.from_numpy(np.load(os.path.join(ROOT, "data", "w_fix.npz"))["w_fix"]).cuda()
-x = torch.from_numpy(d["c3_images"][:10000].reshape(10000, -1).copy()).cuda()
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
+x = torch.from_numpy(d["c3_images"][:n].reshape(n, -1).copy()).cuda()
 evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
 for e in evs:
     e.record(eng.stream)
