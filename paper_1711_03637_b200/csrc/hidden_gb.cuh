@@ -621,15 +621,16 @@ __global__ void __launch_bounds__(kFixThreads) k_hidden_fix(const BatchArgs A) {
 // The same redo with the whole [N][256] table resident in shared memory (one
 // cooperative load per CTA, N <= kResMaxSteps): no per-chunk copies or
 // barriers, so a window's 4 lanes run their N steps back to back.  512
-// threads per CTA, one CTA per SM; a CTA with no flagged window to take
-// returns before loading the table.
+// threads per CTA, one CTA per SM, windows dealt round-robin over the CTAs
+// (the redo list of a small batch still spreads over every SM); a CTA with no
+// flagged window returns before loading the table.
 constexpr int kFixResThreads = 512;
 template <bool SGN, int FZ>
 __global__ void __launch_bounds__(kFixResThreads, 1) k_hidden_fix_res(const BatchArgs A) {
     extern __shared__ __align__(16) double rtab[];  // [N][256]
     const int N = A.c.n_steps;
     const int count = *A.fix_count;
-    if ((int64_t)blockIdx.x * kFixResThreads >= 4LL * count) return;  // CTA-uniform
+    if ((int)blockIdx.x >= count) return;  // CTA-uniform: no flagged window for this CTA
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(A.ctab);
         uint4 *dst = reinterpret_cast<uint4 *>(rtab);
@@ -645,9 +646,13 @@ __global__ void __launch_bounds__(kFixResThreads, 1) k_hidden_fix_res(const Batc
         ts[k] = c_fix_tap[g][k];
         tc[k] = c_fix_tap[8 + g][k];
     }
-    const int nthr = (int)(gridDim.x * kFixResThreads);
-    for (int tb = (int)(blockIdx.x * kFixResThreads); tb < 4 * count; tb += nthr) {  // CTA-uniform
-        const int t = (tb + (int)threadIdx.x) >> 2;  // this quad's window
+    // windows dealt round-robin over the CTAs (quad q of CTA b takes windows
+    // q * G + b, + 128 G, ...), so a short list still spreads over every SM;
+    // a warp whose 8 windows are all past the list skips the pass
+    const int G = (int)gridDim.x, quad = (int)threadIdx.x >> 2, warp = (int)threadIdx.x >> 5;
+    for (int base = 0; base < count; base += (kFixResThreads / 4) * G) {
+        if (base + warp * 8 * G + (int)blockIdx.x >= count) break;  // warp-uniform
+        const int t = base + quad * G + (int)blockIdx.x;  // this quad's window
         const bool have = t < count;
         ItemState it;
         window_setup(A, have, have ? A.fix_list[t] : 0, 0, nchunks, it);
