@@ -664,6 +664,44 @@ __global__ void __launch_bounds__(kFixResThreads, 1) k_hidden_fix_res(const Batc
         for (int ch = 0; ch < nchunks; ++ch) {
             const double *T = rtab + (size_t)ch * kChunk * 256;
             const int nrows = min(kChunk, N - ch * kChunk);
+#ifdef SNN_FIX_PIPE
+            // the chunk's currents first (16 independent 9-tap chains), then the
+            // lane's three membrane chains step by step
+            double Is[kChunk], Ic[kChunk];
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j) {
+                const double *R = T + (j < nrows ? j : 0) * 256;
+                double x[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) x[k] = R[off[k]];
+                Is[j] = __dmul_rn(x[0], ts[0]);
+                Ic[j] = __dmul_rn(x[0], tc[0]);
+#pragma unroll
+                for (int k = 1; k < 9; ++k) {
+                    Is[j] = __fma_rn(x[k], ts[k], Is[j]);
+                    Ic[j] = __fma_rn(x[k], tc[k], Ic[j]);
+                }
+            }
+            // this lane's bits of the chunk's planes: feature g (plane 0), g + 4
+            // (plane 0 for g < 2, else plane 1 bit g - 2), g + 8 (plane 1 bit g + 2)
+            uint64_t p0 = 0, p1 = 0;
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j) {
+                if (j < nrows) {
+                    const uint64_t b0 = fix_lif<SGN, FZ>(Is[j], v0, h0, ph) ? 1u : 0u;
+                    const uint64_t b1 = fix_lif<SGN, FZ>(-Is[j], v1, h1, ph) ? 1u : 0u;
+                    const uint64_t b2 = fix_lif<SGN, FZ>(Ic[j], v2, h2, ph) ? 1u : 0u;
+                    p0 |= b0 << (8 * j + g);
+                    if (g < 2) p0 |= b1 << (8 * j + g + 4);
+                    else p1 |= b1 << (8 * j + g - 2);
+                    p1 |= b2 << (8 * j + g + 2);
+                }
+            }
+            p0 |= __shfl_xor_sync(kFull, p0, 1);
+            p1 |= __shfl_xor_sync(kFull, p1, 1);
+            p0 |= __shfl_xor_sync(kFull, p0, 2);
+            p1 |= __shfl_xor_sync(kFull, p1, 2);
+#else
             uint64_t p0 = 0, p1 = 0;
             for (int j = 0; j < nrows; ++j) {
                 double x[9];
@@ -683,6 +721,7 @@ __global__ void __launch_bounds__(kFixResThreads, 1) k_hidden_fix_res(const Batc
                 p0 |= (uint64_t)(m & 0x3Fu) << (8 * j);
                 p1 |= (uint64_t)(m >> kHalf) << (8 * j);
             }
+#endif
             if (g == 0 && have && it.on) {
                 uint64_t *dst = reinterpret_cast<uint64_t *>(it.rout + (size_t)ch * it.rstride);
                 dst[0] = p0;
