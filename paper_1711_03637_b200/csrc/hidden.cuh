@@ -1132,7 +1132,7 @@ __global__ void __launch_bounds__(kGWarps * 32, SNN_GSUM_MINB) k_gsum(const Batc
 constexpr int kOSteps = 96;
 constexpr int kOutWarps2 = 4;
 
-template <bool TIES>
+template <bool TIES, bool OUTS = true>
 __global__ void __launch_bounds__(kOutWarps2 * 32) k_output(const BatchArgs A, const double *G, const double *Gabs) {
     __shared__ __align__(16) double s_g[kOutWarps2][kOSteps * kNO];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1142,8 +1142,21 @@ __global__ void __launch_bounds__(kOutWarps2 * 32) k_output(const BatchArgs A, c
     const int l = lane < kNO ? lane : kNO - 1;
     const double *Gi = G + (size_t)img * N * kNO;
     double *sg = s_g[warp];
+    // register copies of the step's constants (through a shuffle, so ptxas
+    // cannot re-read them from the constant bank inside the loop)
+    snn_consts_t kc;
+    kc.lif_out = A.c.lif_out;
+    kc.decay_slow = A.c.decay_slow;
+    kc.decay_fast = A.c.decay_fast;
+    kc.inhibition = A.c.inhibition;
+    {
+        double *v[8] = {&kc.lif_out.g, &kc.lif_out.el, &kc.lif_out.vt, &kc.lif_out.beta,
+                        &kc.lif_out.refr, &kc.decay_slow, &kc.decay_fast, &kc.inhibition};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) *v[q] = __shfl_sync(kFull, *v[q], 0);
+    }
     OutState st;
-    out_init(st, A.c);
+    out_init(st, kc);
     const snn_lif_t &p = A.c.lif_out;
     constexpr double kU = 0x1p-53, kTieK = 0x1p-38;
     const double damp = fabs(1.0 - p.beta * p.g);
@@ -1159,7 +1172,7 @@ __global__ void __launch_bounds__(kOutWarps2 * 32) k_output(const BatchArgs A, c
             if (TIES) {
                 TieInfo ti;
                 const double vprev = st.v;
-                const bool fired = out_step(st, A.c, sg[j * kNO + l], s, l, &ff, &ti);
+                const bool fired = out_step(st, kc, sg[j * kNO + l], s, l, &ff, &ti);
                 const double ga = __ldcs(Gabs + ((size_t)img * N + s) * kNO + l);
                 Ab = Ab * A.c.decay_slow + ga;
                 Bb = Bb * A.c.decay_fast + ga;
@@ -1172,12 +1185,14 @@ __global__ void __launch_bounds__(kOutWarps2 * 32) k_output(const BatchArgs A, c
                 if (lane < kNO && ti.live && fabs(ti.vn - p.vt) <= Ev) ++ties;
                 if (!ti.live || fired) Ev = 0.0;  // v == E_L exactly in both
             } else {
-                out_step(st, A.c, sg[j * kNO + l], s, l, &ff);
+                out_step(st, kc, sg[j * kNO + l], s, l, &ff);
             }
-            if (A.out.out_raster && lane == 0) A.out.out_raster[(size_t)img * N + s] = (uint16_t)st.prev;
-            if (lane < kNO) {
-                if (A.out.ff) A.out.ff[((size_t)img * N + s) * kNO + lane] = ff;
-                if (A.out.v_out) A.out.v_out[((size_t)img * N + s) * kNO + lane] = st.v;
+            if (OUTS) {
+                if (A.out.out_raster && lane == 0) A.out.out_raster[(size_t)img * N + s] = (uint16_t)st.prev;
+                if (lane < kNO) {
+                    if (A.out.ff) A.out.ff[((size_t)img * N + s) * kNO + lane] = ff;
+                    if (A.out.v_out) A.out.v_out[((size_t)img * N + s) * kNO + lane] = st.v;
+                }
             }
         }
         __syncwarp();

@@ -379,7 +379,8 @@ int launch_contract(const BatchArgs &A, double *g, cudaStream_t st) {
         if (A.out.out_raster || A.out.ff || A.out.v_out) k_output_dist<true><<<og, kOutWarps2 * 32, 0, st>>>(A, g);
         else k_output_dist<false><<<og, kOutWarps2 * 32, 0, st>>>(A, g);
     }
-    else k_output<false><<<og, kOutWarps2 * 32, 0, st>>>(A, g, nullptr);
+    else if (A.out.out_raster || A.out.ff || A.out.v_out) k_output<false, true><<<og, kOutWarps2 * 32, 0, st>>>(A, g, nullptr);
+    else k_output<false, false><<<og, kOutWarps2 * 32, 0, st>>>(A, g, nullptr);
     stage_mark(5, st);
     return cuda_check("k_output");
 }
