@@ -1129,7 +1129,10 @@ __global__ void __launch_bounds__(kGWarps * 32, SNN_GSUM_MINB) k_gsum(const Batc
 // (magnitudes of the LIF's operands), reset to 0 whenever v is E_L in both
 // (spike or refractory).  A step of a live neuron with |vn - V_T| <= Ev is a
 // near tie: only there can the reference's threshold decision differ.
-constexpr int kOSteps = 96;
+#ifndef SNN_OSTEPS
+#define SNN_OSTEPS 96
+#endif
+constexpr int kOSteps = SNN_OSTEPS;  // G rows staged per round (one round for N <= kOSteps)
 constexpr int kOutWarps2 = 4;
 
 template <bool TIES, bool OUTS = true>
