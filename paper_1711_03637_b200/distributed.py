@@ -82,4 +82,7 @@ def sharded_batch_counts(images, weights, filters, cfg, group=None) -> np.ndarra
             local = torch.zeros((0, N_OUTPUTS), dtype=torch.int32, device=eng.device)
         eng.stream.synchronize()
     allc = gather_counts(local, n, group)
-    return allc.cpu().numpy().astype(np.int64)
+    from .api import _fetch
+    torch.cuda.current_stream(eng.device).synchronize()  # the gather ran on the caller's stream
+    with eng.lock:
+        return _fetch(eng, allc, np.int64)  # one DMA through the engine's pinned staging buffer

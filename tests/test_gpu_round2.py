@@ -372,3 +372,18 @@ def test_guard_band_long_trial_chunked_redo(sd, cfg, bank, workloads, wfix):
     assert res[1][1].any()
     assert np.array_equal(res[1][0], res[3][0])
     assert np.array_equal(res[1][1], res[3][1])
+
+
+def test_sharded_batch_counts_two_ranks_one_gpu():
+    """distributed.sharded_batch_counts (the multi-GPU e2e path of bench.py)
+    with two ranks sharing one GPU over gloo: its counts equal batch_counts'
+    (scripts/sharded_check.py under torchrun)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29541",
+                        os.path.join(ROOT, "scripts", "sharded_check.py")],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.stdout.count("sharded == batch_counts: True") == 2
