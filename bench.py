@@ -747,8 +747,10 @@ def critical_path_model(c):
     scan = 0.77 * (6 * lat + 25) + 0.23 * (14 * lat + 25)
     adj = 2 * lat
     cyc = n * scan
+    scan_meas = 228.0  # cycles per step of the speculative scan, clock-stamped (scripts/scan_stamps.py)
     return {"model_us_per_image": cyc / 1965.0, "scan_cycles_per_step": scan,
             "adjoint_cycles_per_step_off_chain": adj, "n_steps": n, "clock_mhz": 1965,
+            "scan_measured_cycles_per_step": scan_meas, "scan_measured_us_per_image": n * scan_meas / 1965.0,
             "basis": "dependent-chain latency only (FP64 8.2 cycles); measured scan: 228 cycles/step, issue-bound "
                      "single warp of ~160 instructions per step (scripts/scan_stamps.py)"}
 
@@ -844,7 +846,9 @@ def bench_train(args, sd, eng, d, cfg, bank):
             "dense_equiv_tflops": value * (F_TRAIN_PER_STEP * 100 + F_TRAIN_PER_IMAGE) / 1e12,
             "gpu_launches_per_epoch": train_launches(eng, c, n),
             "critical_path": dict(critical_path_model(c), frac_of_measured=critical_path_model(c)[
-                "model_us_per_image"] / (statistics.median(times) * 1e3 / n)),
+                "model_us_per_image"] / (statistics.median(times) * 1e3 / n),
+                scan_share_of_measured=critical_path_model(c)["scan_measured_us_per_image"] /
+                (statistics.median(times) * 1e3 / n)),
             "kernels": train_kernel_table(),
             "cpu_baseline": {"value": cpu, "unit": "images/s", "cores": 1, "kind": kind, "sample": desc}}
 
